@@ -1,0 +1,129 @@
+/*
+ * dfx.h — C ABI of the B200-native DoRA hot path (libdfx.so).
+ *
+ * This is the drop-in boundary.  Every entry point replaces one function of the
+ * reference C++ API (/root/reference/proj/include/dorafactor/, cited per entry)
+ * with a device-pointer, caller-owned-buffer, stream-ordered equivalent.  The C++
+ * drop-in (include/dorafactor/ headers, libdorafactor_b200.so) implements the
+ * reference signatures on top of these calls; other hosts bind them directly
+ * (ctypes / cgo / JNI stubs in INTEGRATION.md).
+ *
+ * Conventions
+ *   - Matrices are dense row-major device arrays of the call's dtype (fp32, bf16 or
+ *     fp16 bits).  Per-row vectors (g, w_norm, m, terms, d_mag) are fp32 device
+ *     arrays; where the reference rounds a vector to the working dtype the fp32
+ *     array holds the rounded (exactly representable) value.
+ *   - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default).
+ *     They never allocate on the hot path except to grow the context workspace on
+ *     first use of a larger shape, and never synchronise the device.
+ *   - Return value: DFX_OK, or an error code with a message in dfx_last_error()
+ *     (thread-local).  DFX_EINVAL is raised exactly where the reference throws
+ *     std::invalid_argument.  Non-finite values propagate (IEEE), never error.
+ *   - A context is bound to one device; concurrent calls on one context must be
+ *     serialised by the caller (its workspace is shared).  Use one context per
+ *     concurrently used stream.
+ *   - There is no CPU fallback: every call runs sm_100a kernels and fails with
+ *     DFX_ENODEV when no usable device is present.
+ */
+#ifndef DFX_H
+#define DFX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* dfx_stream_t; /* == cudaStream_t */
+typedef struct dfx_ctx dfx_ctx;
+
+typedef enum dfx_dtype {
+    DFX_F32 = 0,  /* DTypeKind::FP32  (dtype.hpp:12) */
+    DFX_BF16 = 1, /* DTypeKind::BF16E */
+    DFX_F16 = 2   /* DTypeKind::FP16E */
+} dfx_dtype;
+
+enum {
+    DFX_OK = 0,
+    DFX_EINVAL = 1,      /* reference would throw std::invalid_argument */
+    DFX_ECUDA = 2,       /* CUDA runtime / driver error */
+    DFX_ENOMEM = 3,      /* workspace allocation failed */
+    DFX_ENODEV = 4,      /* no sm_100 device / context for another device */
+    DFX_EUNSUPPORTED = 5 /* dtype not handled by this entry point */
+};
+
+#define DFX_ABI_VERSION 1
+
+int dfx_abi_version(void);
+const char* dfx_last_error(void);
+
+/* Context: device binding + grow-only workspace (Gram partials, bf16 hi/lo Gram,
+ * per-split row partials). */
+int dfx_ctx_create(int device, dfx_ctx** out);
+void dfx_ctx_destroy(dfx_ctx* ctx);
+/* Number of kernels launched by this context since creation (evidence counter). */
+int64_t dfx_ctx_launches(const dfx_ctx* ctx);
+
+/* plan_chunks (matrix.hpp:68, matrix.cpp:28-51): host-only, no device needed.
+ * DFX_EINVAL where the reference throws. */
+int dfx_plan_chunks(uint64_t d_out, uint64_t d_in, uint64_t budget_bytes,
+                    uint64_t* chunk_size, uint64_t* num_chunks);
+
+/* factored_norm_terms (factored_norm.hpp:44): base_sq / cross / ba_sq for
+ * ||W + sBA||^2_row.  W [d_out x d_in], A [r x d_in], B [d_out x r] (dtype).
+ * chunk_size is ChunkPlan::chunk_size (base_sq chunk-partial semantics).
+ * Outputs are fp32 [d_out]; any of them may be NULL. */
+int dfx_norm_terms(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A, const void* B,
+                   int64_t d_out, int64_t d_in, int64_t r, double s, int64_t chunk_size,
+                   float* base_sq, float* cross, float* ba_sq, dfx_stream_t stream);
+
+/* assemble_norm (factored_norm.hpp:51) when round_to == DFX_F32; with round_to =
+ * BF16/F16 additionally the round_to_dtype of factored_row_norm (:213-215). */
+int dfx_assemble_norm(dfx_ctx* ctx, const float* base_sq, const float* cross,
+                      const float* ba_sq, double two_s, double s2, int64_t n,
+                      dfx_dtype round_to, float* w_norm, dfx_stream_t stream);
+
+/* magnitude_scale (factored_norm.hpp:63-64), non-fp64 working dtype:
+ * g = round_dtype(fl32(m) / max(fl32(w_norm), fl32(eps_dtype))). */
+int dfx_magnitude_scale(dfx_ctx* ctx, dfx_dtype dtype, const float* m, const float* w_norm,
+                        int64_t n, float* g, dfx_stream_t stream);
+
+/* factored_row_norm (factored_norm.hpp:57-58) fused with magnitude_scale: one launch
+ * sequence producing w_norm (rounded to `dtype`) and, when m != NULL, g (rounded to
+ * `mag_dtype`).  terms (3 x d_out fp32: base_sq, cross, ba_sq) may be NULL. */
+int dfx_row_norm(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A, const void* B,
+                 int64_t d_out, int64_t d_in, int64_t r, double s, int64_t chunk_size,
+                 const float* m, dfx_dtype mag_dtype, float* w_norm, float* g, float* terms,
+                 dfx_stream_t stream);
+
+/* stable_compose / fused_compose / dual_output_compose (compose.hpp:43,53-57,62-68):
+ * delta = (g-1)*base + g*(s*lora) in the canonical rounding order, bitwise equal to
+ * the reference; inner = s*lora + base when inner != NULL (dual output). */
+int dfx_compose_fwd(dfx_ctx* ctx, dfx_dtype dtype, const void* base, const void* lora,
+                    const float* g, double s, int64_t rows, int64_t d_out, void* delta,
+                    void* inner, dfx_stream_t stream);
+
+/* compose_backward (compose.hpp:73-75): d_lora = g*s*dY, d_base = (g-1)*dY; when
+ * d_mag != NULL (mag_grad) also d_mag = serial-per-column sum(dY*inner) / w_norm,
+ * bitwise equal to the reference's fixed serial order.  inner/w_norm required then. */
+int dfx_compose_bwd(dfx_ctx* ctx, dfx_dtype dtype, const void* dy, const float* g, double s,
+                    const void* inner, const float* w_norm, int64_t rows, int64_t d_out,
+                    void* d_lora, void* d_base, float* d_mag, dfx_stream_t stream);
+
+/* One whole DoRA module forward from HOST buffers (the end-to-end call a host
+ * framework makes): H2D of W, A, B, m, base, lora; row norm + g; compose; D2H of
+ * delta and g.  Host buffers should be pinned for full PCIe bandwidth.  Blocks
+ * until the results are in host memory. */
+int dfx_module_fwd_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A,
+                        const void* B, const float* m, const void* base, const void* lora,
+                        double s, int64_t d_out, int64_t d_in, int64_t r, int64_t rows,
+                        int64_t chunk_size, void* delta, float* g);
+
+/* 1 when dfx_row_norm takes the tcgen05/TMA path for this (dtype, shape). */
+int dfx_norm_uses_tensor_cores(dfx_dtype dtype, int64_t d_out, int64_t d_in, int64_t r);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DFX_H */

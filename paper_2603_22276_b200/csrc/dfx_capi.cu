@@ -1,0 +1,449 @@
+// dfx_capi.cu — the C ABI (include/dfx.h): context, validation, orchestration.
+//
+// Validation mirrors the reference's throw sites so the C++ drop-in can map
+// DFX_EINVAL back to std::invalid_argument one-for-one:
+//   factored_norm.cpp:11-23 (shapes, rank, plan), :28-30 (FP64 weights)
+//   factored_norm.cpp:124-126 (assemble length), :221-223 (magnitude length)
+//   compose.cpp:9-16 (base/lora/g shapes), :72-75 (contiguity, host side),
+//   compose.cpp:158-169 (backward: g length, inner required/shape, w_norm length)
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dfx.h"
+#include "kernels/launch.h"
+
+namespace dfx {
+
+struct Workspace {
+    int device = 0;
+    std::vector<void*> ptr;
+    std::vector<size_t> cap;
+    Workspace() : ptr(16, nullptr), cap(16, 0) {}
+    ~Workspace() {
+        for (void* p : ptr)
+            if (p) cudaFree(p);
+    }
+};
+
+void* ws_get(Workspace* ws, int slot, size_t bytes, cudaError_t* err) {
+    *err = cudaSuccess;
+    if (bytes == 0) bytes = 16;
+    if (ws->cap[slot] >= bytes) return ws->ptr[slot];
+    if (ws->ptr[slot]) {
+        // the old buffer may still be read by queued work on any stream
+        cudaDeviceSynchronize();
+        cudaFree(ws->ptr[slot]);
+        ws->ptr[slot] = nullptr;
+        ws->cap[slot] = 0;
+    }
+    const size_t want = bytes + bytes / 4;
+    *err = cudaMalloc(&ws->ptr[slot], want);
+    if (*err != cudaSuccess) {
+        ws->ptr[slot] = nullptr;
+        return nullptr;
+    }
+    ws->cap[slot] = want;
+    return ws->ptr[slot];
+}
+
+namespace {
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+    static EncodeFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<EncodeFn>(nullptr);
+        return reinterpret_cast<EncodeFn>(p);
+    }();
+    return fn;
+}
+}  // namespace
+
+cudaError_t make_tmap_2d(CUtensorMap* out, int dt, const void* base, uint64_t rows, uint64_t cols,
+                         uint64_t row_pitch_bytes, uint32_t box_cols, uint32_t box_rows,
+                         bool swizzle128) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    const CUtensorMapDataType t = dt == kF32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                  : dt == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {row_pitch_bytes};
+    const cuuint32_t box[2] = {box_cols, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(out, t, 2, const_cast<void*>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+}  // namespace dfx
+
+struct dfx_ctx {
+    int device = 0;
+    dfx::Workspace ws;
+    int64_t launches = 0;
+    // module_fwd_host staging
+    cudaStream_t st_h2d = nullptr, st_comp = nullptr, st_d2h = nullptr;
+    std::vector<void*> stage;
+    std::vector<size_t> stage_cap;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(DFX_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+bool valid_dtype(int dt) { return dt == DFX_F32 || dt == DFX_BF16 || dt == DFX_F16; }
+
+// Binds the calling thread to the context's device.
+int enter(dfx_ctx* ctx) {
+    if (!ctx) return fail(DFX_EINVAL, "null context");
+    const cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    return DFX_OK;
+}
+
+int finish_call(cudaError_t e, const char* where) {
+    if (e != cudaSuccess) return cuda_fail(e, where);
+    g_err.clear();
+    return DFX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dfx_abi_version(void) { return DFX_ABI_VERSION; }
+
+const char* dfx_last_error(void) { return g_err.c_str(); }
+
+int dfx_ctx_create(int device, dfx_ctx** out) {
+    if (!out) return fail(DFX_EINVAL, "dfx_ctx_create: null out");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(DFX_ENODEV, "dfx_ctx_create: no CUDA device (%s)",
+                    e == cudaSuccess ? "count 0" : cudaGetErrorString(e));
+    if (device < 0 || device >= n) return fail(DFX_EINVAL, "dfx_ctx_create: bad device %d", device);
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(DFX_ENODEV, "dfx: built for sm_100a, device %d is sm_%d%d", device, prop.major,
+                    prop.minor);
+    e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    dfx_ctx* c = new dfx_ctx();
+    c->device = device;
+    c->ws.device = device;
+    c->stage.assign(16, nullptr);
+    c->stage_cap.assign(16, 0);
+    *out = c;
+    g_err.clear();
+    return DFX_OK;
+}
+
+void dfx_ctx_destroy(dfx_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    for (void* p : ctx->stage)
+        if (p) cudaFree(p);
+    if (ctx->st_h2d) cudaStreamDestroy(ctx->st_h2d);
+    if (ctx->st_comp) cudaStreamDestroy(ctx->st_comp);
+    if (ctx->st_d2h) cudaStreamDestroy(ctx->st_d2h);
+    delete ctx;
+}
+
+int64_t dfx_ctx_launches(const dfx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int dfx_plan_chunks(uint64_t d_out, uint64_t d_in, uint64_t budget, uint64_t* chunk_size,
+                    uint64_t* num_chunks) {
+    // matrix.cpp:28-51
+    if (d_out < 1 || d_in < 1) return fail(DFX_EINVAL, "plan_chunks: dims must be >= 1");
+    if (budget < 256) return fail(DFX_EINVAL, "plan_chunks: budget below 256 bytes");
+    const uint64_t align = 64;
+    const uint64_t fit = budget / (d_out * 4);
+    if (d_in >= align && fit < align)
+        return fail(DFX_EINVAL,
+                    "plan_chunks: budget of %llu bytes cannot hold one 64-wide fp32 chunk at "
+                    "d_out=%llu",
+                    (unsigned long long)budget, (unsigned long long)d_out);
+    uint64_t cs = d_in < fit ? d_in : fit;
+    cs = (cs / align) * align;
+    const uint64_t floor_cs = d_in < align ? d_in : align;
+    if (cs < floor_cs) cs = floor_cs;
+    if (chunk_size) *chunk_size = cs;
+    if (num_chunks) *num_chunks = (d_in + cs - 1) / cs;
+    g_err.clear();
+    return DFX_OK;
+}
+
+int dfx_norm_uses_tensor_cores(dfx_dtype dtype, int64_t d_out, int64_t d_in, int64_t r) {
+    return dfx::norm_uses_tensor_cores(dtype, d_out, d_in, r);
+}
+
+static int check_norm_args(dfx_dtype dtype, const void* W, const void* A, const void* B,
+                           int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size) {
+    if (!valid_dtype(dtype))
+        return fail(DFX_EINVAL,
+                    "factored_norm_terms: fp32 term accumulation requires non-FP64 weights");
+    if (d_out < 0 || d_in < 0) return fail(DFX_EINVAL, "factored_norm: negative dims");
+    if (r < 1) return fail(DFX_EINVAL, "factored_norm: rank must be >= 1");
+    if (chunk_size < 1) return fail(DFX_EINVAL, "factored_norm: chunk plan does not match W.cols");
+    if (d_out > 0 && d_in > 0 && (!W || !A || !B))
+        return fail(DFX_EINVAL, "factored_norm: null operand");
+    return DFX_OK;
+}
+
+static int run_norm(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A, const void* B,
+                    int64_t d_out, int64_t d_in, int64_t r, double s, int64_t chunk_size,
+                    float* base_sq, float* cross, float* ba_sq, const float* m,
+                    dfx_dtype mag_dtype, float* w_norm, float* g, int round_dt,
+                    cudaStream_t st, const char* where) {
+    dfx::NormArgs a{};
+    a.dt = dtype; a.w = W; a.a = A; a.b = B;
+    a.d_out = d_out; a.d_in = d_in; a.r = r; a.s = s; a.chunk_size = chunk_size;
+    a.base_sq = base_sq; a.cross = cross; a.ba_sq = ba_sq;
+    a.m = m; a.w_norm = w_norm; a.g = g;
+    a.round_dt = round_dt; a.mag_dt = mag_dtype;
+    int launches = 0;
+    const cudaError_t e = dfx::launch_norm(a, &ctx->ws, st, &launches);
+    ctx->launches += launches;
+    return finish_call(e, where);
+}
+
+int dfx_norm_terms(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A, const void* B,
+                   int64_t d_out, int64_t d_in, int64_t r, double s, int64_t chunk_size,
+                   float* base_sq, float* cross, float* ba_sq, dfx_stream_t stream) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    rc = check_norm_args(dtype, W, A, B, d_out, d_in, r, chunk_size);
+    if (rc) return rc;
+    return run_norm(ctx, dtype, W, A, B, d_out, d_in, r, s, chunk_size, base_sq, cross, ba_sq,
+                    nullptr, DFX_F32, nullptr, nullptr, dfx::kF32, stream, "dfx_norm_terms");
+}
+
+int dfx_row_norm(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A, const void* B,
+                 int64_t d_out, int64_t d_in, int64_t r, double s, int64_t chunk_size,
+                 const float* m, dfx_dtype mag_dtype, float* w_norm, float* g, float* terms,
+                 dfx_stream_t stream) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    rc = check_norm_args(dtype, W, A, B, d_out, d_in, r, chunk_size);
+    if (rc) return rc;
+    if (m && !valid_dtype(mag_dtype)) return fail(DFX_EUNSUPPORTED, "dfx_row_norm: mag dtype");
+    if (m && !g) return fail(DFX_EINVAL, "dfx_row_norm: m given without g output");
+    float* bs = terms ? terms : nullptr;
+    float* cr = terms ? terms + d_out : nullptr;
+    float* bq = terms ? terms + 2 * d_out : nullptr;
+    return run_norm(ctx, dtype, W, A, B, d_out, d_in, r, s, chunk_size, bs, cr, bq, m, mag_dtype,
+                    w_norm, g, dtype, stream, "dfx_row_norm");
+}
+
+int dfx_assemble_norm(dfx_ctx* ctx, const float* base_sq, const float* cross,
+                      const float* ba_sq, double two_s, double s2, int64_t n,
+                      dfx_dtype round_to, float* w_norm, dfx_stream_t stream) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (n < 0) return fail(DFX_EINVAL, "assemble_norm: term vectors differ in length");
+    if (!valid_dtype(round_to)) return fail(DFX_EUNSUPPORTED, "assemble_norm: dtype");
+    if (n > 0 && (!base_sq || !cross || !ba_sq || !w_norm))
+        return fail(DFX_EINVAL, "assemble_norm: null vector");
+    int launches = 0;
+    const cudaError_t e = dfx::launch_assemble(base_sq, cross, ba_sq, two_s, s2, n, round_to,
+                                               w_norm, stream, &launches);
+    ctx->launches += launches;
+    return finish_call(e, "dfx_assemble_norm");
+}
+
+int dfx_magnitude_scale(dfx_ctx* ctx, dfx_dtype dtype, const float* m, const float* w_norm,
+                        int64_t n, float* g, dfx_stream_t stream) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (!valid_dtype(dtype)) return fail(DFX_EUNSUPPORTED, "magnitude_scale: fp64 is host-only");
+    if (n < 0) return fail(DFX_EINVAL, "magnitude_scale: length mismatch");
+    if (n > 0 && (!m || !w_norm || !g)) return fail(DFX_EINVAL, "magnitude_scale: null vector");
+    int launches = 0;
+    const cudaError_t e = dfx::launch_magnitude_scale(dtype, m, w_norm, n, g, stream, &launches);
+    ctx->launches += launches;
+    return finish_call(e, "dfx_magnitude_scale");
+}
+
+int dfx_compose_fwd(dfx_ctx* ctx, dfx_dtype dtype, const void* base, const void* lora,
+                    const float* g, double s, int64_t rows, int64_t d_out, void* delta,
+                    void* inner, dfx_stream_t stream) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (!valid_dtype(dtype)) return fail(DFX_EUNSUPPORTED, "compose: dtype");
+    if (rows < 0 || d_out < 0) return fail(DFX_EINVAL, "compose: base/lora shapes differ");
+    if (rows > 0 && d_out > 0 && (!base || !lora || !g || !delta))
+        return fail(DFX_EINVAL, "compose: null operand");
+    int launches = 0;
+    const cudaError_t e =
+        dfx::launch_compose_fwd(dtype, base, lora, g, static_cast<float>(s), rows, d_out, delta,
+                                inner, stream, &launches);
+    ctx->launches += launches;
+    return finish_call(e, "dfx_compose_fwd");
+}
+
+int dfx_compose_bwd(dfx_ctx* ctx, dfx_dtype dtype, const void* dy, const float* g, double s,
+                    const void* inner, const float* w_norm, int64_t rows, int64_t d_out,
+                    void* d_lora, void* d_base, float* d_mag, dfx_stream_t stream) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (!valid_dtype(dtype)) return fail(DFX_EUNSUPPORTED, "compose_backward: dtype");
+    if (rows < 0 || d_out < 0) return fail(DFX_EINVAL, "compose_backward: g length != d_out");
+    if (d_mag && !inner)
+        return fail(DFX_EINVAL, "compose_backward: magnitude gradient requires inner");
+    if (d_mag && !w_norm) return fail(DFX_EINVAL, "compose_backward: w_norm length != d_out");
+    if (rows > 0 && d_out > 0 && (!dy || !g || !d_lora || !d_base))
+        return fail(DFX_EINVAL, "compose_backward: null operand");
+    int launches = 0;
+    const cudaError_t e =
+        dfx::launch_compose_bwd(dtype, dy, g, static_cast<float>(s), inner, w_norm, rows, d_out,
+                                d_lora, d_base, d_mag, stream, &launches);
+    ctx->launches += launches;
+    return finish_call(e, "dfx_compose_bwd");
+}
+
+static void* stage_buf(dfx_ctx* ctx, int slot, size_t bytes, cudaError_t* e) {
+    *e = cudaSuccess;
+    if (bytes == 0) bytes = 16;
+    if (ctx->stage_cap[slot] >= bytes) return ctx->stage[slot];
+    if (ctx->stage[slot]) {
+        cudaDeviceSynchronize();
+        cudaFree(ctx->stage[slot]);
+    }
+    ctx->stage[slot] = nullptr;
+    ctx->stage_cap[slot] = 0;
+    *e = cudaMalloc(&ctx->stage[slot], bytes);
+    if (*e != cudaSuccess) return nullptr;
+    ctx->stage_cap[slot] = bytes;
+    return ctx->stage[slot];
+}
+
+int dfx_module_fwd_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A,
+                        const void* B, const float* m, const void* base, const void* lora,
+                        double s, int64_t d_out, int64_t d_in, int64_t r, int64_t rows,
+                        int64_t chunk_size, void* delta, float* g) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    rc = check_norm_args(dtype, W, A, B, d_out, d_in, r, chunk_size);
+    if (rc) return rc;
+    if (rows < 0 || !m || !g || (rows > 0 && (!base || !lora || !delta)))
+        return fail(DFX_EINVAL, "dfx_module_fwd_host: null operand");
+    cudaError_t e = cudaSuccess;
+    if (!ctx->st_h2d) {
+        if ((e = cudaStreamCreateWithFlags(&ctx->st_h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&ctx->st_comp, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&ctx->st_d2h, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e, "stream create");
+    }
+    const size_t eb = dtype == DFX_F32 ? 4 : 2;
+    const size_t nW = size_t(d_out) * d_in, nA = size_t(r) * d_in, nB = size_t(d_out) * r;
+    const size_t nact = size_t(rows) * d_out;
+    void* dW = stage_buf(ctx, 0, nW * eb, &e);
+    if (e) return cuda_fail(e, "stage alloc");
+    void* dA = stage_buf(ctx, 1, nA * eb, &e);
+    if (e) return cuda_fail(e, "stage alloc");
+    void* dB = stage_buf(ctx, 2, nB * eb, &e);
+    if (e) return cuda_fail(e, "stage alloc");
+    float* dm = static_cast<float*>(stage_buf(ctx, 3, d_out * 4, &e));
+    if (e) return cuda_fail(e, "stage alloc");
+    float* dg = static_cast<float*>(stage_buf(ctx, 4, d_out * 4, &e));
+    if (e) return cuda_fail(e, "stage alloc");
+    float* dwn = static_cast<float*>(stage_buf(ctx, 5, d_out * 4, &e));
+    if (e) return cuda_fail(e, "stage alloc");
+    void* dbase = stage_buf(ctx, 6, nact * eb, &e);
+    if (e) return cuda_fail(e, "stage alloc");
+    void* dlora = stage_buf(ctx, 7, nact * eb, &e);
+    if (e) return cuda_fail(e, "stage alloc");
+    void* ddelta = stage_buf(ctx, 8, nact * eb, &e);
+    if (e) return cuda_fail(e, "stage alloc");
+
+    cudaEvent_t ev_norm, ev_w;
+    cudaEventCreateWithFlags(&ev_norm, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_w, cudaEventDisableTiming);
+    // weights first: the norm overlaps the activation upload
+    cudaMemcpyAsync(dA, A, nA * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
+    cudaMemcpyAsync(dB, B, nB * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
+    cudaMemcpyAsync(dm, m, d_out * 4, cudaMemcpyHostToDevice, ctx->st_h2d);
+    cudaMemcpyAsync(dW, W, nW * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
+    cudaEventRecord(ev_w, ctx->st_h2d);
+    cudaStreamWaitEvent(ctx->st_comp, ev_w, 0);
+    rc = run_norm(ctx, dtype, dW, dA, dB, d_out, d_in, r, s, chunk_size, nullptr, nullptr,
+                  nullptr, dm, dtype, dwn, dg, dtype, ctx->st_comp, "dfx_module_fwd_host/norm");
+    if (rc) return rc;
+    cudaEventRecord(ev_norm, ctx->st_comp);
+    cudaStreamWaitEvent(ctx->st_d2h, ev_norm, 0);
+    cudaMemcpyAsync(g, dg, d_out * 4, cudaMemcpyDeviceToHost, ctx->st_d2h);
+
+    // activations in row chunks: upload chunk c+1 while composing c and downloading c-1
+    const int64_t nchunk = rows >= 1024 ? 8 : 1;
+    const int64_t crow = (rows + nchunk - 1) / nchunk;
+    std::vector<cudaEvent_t> evs;
+    for (int64_t r0 = 0; r0 < rows; r0 += crow) {
+        const int64_t nr = std::min(crow, rows - r0);
+        const size_t off = size_t(r0) * d_out * eb, bytes = size_t(nr) * d_out * eb;
+        cudaEvent_t ein, eout;
+        cudaEventCreateWithFlags(&ein, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&eout, cudaEventDisableTiming);
+        evs.push_back(ein);
+        evs.push_back(eout);
+        cudaMemcpyAsync(static_cast<char*>(dbase) + off, static_cast<const char*>(base) + off,
+                        bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        cudaMemcpyAsync(static_cast<char*>(dlora) + off, static_cast<const char*>(lora) + off,
+                        bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        cudaEventRecord(ein, ctx->st_h2d);
+        cudaStreamWaitEvent(ctx->st_comp, ein, 0);
+        int launches = 0;
+        e = dfx::launch_compose_fwd(dtype, static_cast<char*>(dbase) + off,
+                                    static_cast<char*>(dlora) + off, dg, static_cast<float>(s), nr,
+                                    d_out, static_cast<char*>(ddelta) + off, nullptr, ctx->st_comp,
+                                    &launches);
+        ctx->launches += launches;
+        if (e != cudaSuccess) return cuda_fail(e, "dfx_module_fwd_host/compose");
+        cudaEventRecord(eout, ctx->st_comp);
+        cudaStreamWaitEvent(ctx->st_d2h, eout, 0);
+        cudaMemcpyAsync(static_cast<char*>(delta) + off, static_cast<char*>(ddelta) + off, bytes,
+                        cudaMemcpyDeviceToHost, ctx->st_d2h);
+    }
+    e = cudaStreamSynchronize(ctx->st_d2h);
+    cudaEventDestroy(ev_norm);
+    cudaEventDestroy(ev_w);
+    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return finish_call(e, "dfx_module_fwd_host");
+}
+
+}  // extern "C"

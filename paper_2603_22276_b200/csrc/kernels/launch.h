@@ -1,0 +1,66 @@
+// launch.h — internal launcher interface between the C-ABI layer (dfx_capi.cu) and the
+// kernel translation units.  Not installed; the public boundary is include/dfx.h.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace dfx {
+
+enum DType : int { kF32 = 0, kBF16 = 1, kF16 = 2 };
+
+inline int elem_bytes(int dt) { return dt == kF32 ? 4 : 2; }
+
+// Encodes a 2-D row-major tensor map (rows x cols elements, row pitch in bytes)
+// with the given box; swizzle128 selects CU_TENSOR_MAP_SWIZZLE_128B.
+// Returns cudaSuccess or an error (driver entry point missing / encode failure).
+cudaError_t make_tmap_2d(CUtensorMap* out, int dt, const void* base, uint64_t rows, uint64_t cols,
+                         uint64_t row_pitch_bytes, uint32_t box_cols, uint32_t box_rows,
+                         bool swizzle128);
+
+// ---------------------------------------------------------------- compose
+cudaError_t launch_compose_fwd(int dt, const void* base, const void* lora, const float* g, float sf,
+                               int64_t rows, int64_t d_out, void* delta, void* inner,
+                               cudaStream_t st, int* launches);
+
+cudaError_t launch_compose_bwd(int dt, const void* dy, const float* g, float sf, const void* inner,
+                               const float* w_norm, int64_t rows, int64_t d_out, void* d_lora,
+                               void* d_base, float* d_mag, cudaStream_t st, int* launches);
+
+// ------------------------------------------------------------------- norm
+struct NormArgs {
+    int dt;
+    const void* w;
+    const void* a;
+    const void* b;
+    int64_t d_out, d_in, r;
+    double s;
+    int64_t chunk_size;
+    // outputs (device): any of these may be null except where noted
+    float* base_sq;
+    float* cross;
+    float* ba_sq;
+    const float* m;   // magnitude (fp32), null => no g
+    float* w_norm;    // dtype-rounded norm (fp32 storage)
+    float* g;         // dtype-rounded scale (fp32 storage)
+    int round_dt;     // dtype the norm is rounded to (kF32 => plain fp32 assemble)
+    int mag_dt;       // working dtype of the magnitude division
+};
+
+struct Workspace;  // owned by the context (dfx_capi.cu)
+void* ws_get(Workspace* ws, int slot, size_t bytes, cudaError_t* err);
+
+cudaError_t launch_norm(const NormArgs& a, Workspace* ws, cudaStream_t st, int* launches);
+
+cudaError_t launch_assemble(const float* base_sq, const float* cross, const float* ba_sq,
+                            double two_s, double s2, int64_t n, int round_dt, float* out,
+                            cudaStream_t st, int* launches);
+
+cudaError_t launch_magnitude_scale(int dt, const float* m, const float* w_norm, int64_t n,
+                                   float* g, cudaStream_t st, int* launches);
+
+// Chooses the tensor-core path for (dt, shape); exposed for tests/bench reporting.
+int norm_uses_tensor_cores(int dt, int64_t d_out, int64_t d_in, int64_t r);
+
+}  // namespace dfx

@@ -1,0 +1,232 @@
+"""GPU parity of the factored row norm + magnitude scale against the CPU oracle (pinned
+to the reference by tests/test_oracle.py), the reference's own golden vectors, and the
+fp64 dense ground truth.
+
+Bars (BASELINE north_star): row norms within 1e-5 relative in fp32 and 1e-2 in bf16.
+fp32 rows with heavy cancellation (kappa = (base+|2s cross|+s^2 ba)/norm^2 large) are
+held to max(1e-5, 64*kappa*2^-24), the bound the reference itself needs.
+Bitwise where the reference's arithmetic is order-fixed: base_sq (serial chain per
+ChunkPlan chunk), assemble_norm, magnitude_scale."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import bits_equal, to_dev, to_np
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _terms(dfx, W, A, B, s, cs, dt):
+    import torch
+    w, a, b = to_dev(W, dt), to_dev(A, dt), to_dev(B, dt)
+    out = torch.empty(3, W.shape[0], dtype=torch.float32, device="cuda")
+    dfx.norm_terms(w, a, b, s, cs, out[0], out[1], out[2])
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    return o[0], o[1], o[2]
+
+
+def _row_norm(dfx, W, A, B, s, cs, dt, m=None):
+    import torch
+    w, a, b = to_dev(W, dt), to_dev(A, dt), to_dev(B, dt)
+    wn = torch.empty(W.shape[0], dtype=torch.float32, device="cuda")
+    g = torch.empty_like(wn) if m is not None else None
+    md = torch.from_numpy(np.asarray(m, np.float32)).cuda() if m is not None else None
+    terms = torch.empty(3, W.shape[0], dtype=torch.float32, device="cuda")
+    dfx.row_norm(w, a, b, s, cs, wn, m=md, g=g, terms=terms)
+    torch.cuda.synchronize()
+    return wn.cpu().numpy(), (g.cpu().numpy() if g is not None else None), terms.cpu().numpy()
+
+
+def _kappa(o, W, A, B, s):
+    # fp64 terms via the dense route on small shapes
+    BA = B.astype(np.float64) @ A.astype(np.float64)
+    W64 = W.astype(np.float64)
+    base = (W64 * W64).sum(1)
+    cross = (W64 * BA).sum(1)
+    ba = (BA * BA).sum(1)
+    n2 = base + 2 * s * cross + s * s * ba
+    return (base + np.abs(2 * s * cross) + s * s * ba) / np.maximum(n2, 1e-300)
+
+
+def _fixture(o, d_out, d_in, r, seed, dt=0):
+    W = o.seeded_gaussian(d_out, d_in, o.derive_seed(seed, 0), dt)
+    A = o.seeded_gaussian(r, d_in, o.derive_seed(seed, 1), dt)
+    B = o.seeded_gaussian(d_out, r, o.derive_seed(seed, 2), dt)
+    return W, A, B
+
+
+def test_known_answers(dfx, oracle):
+    W = np.zeros((2, 2), np.float32)
+    A = np.array([[3, 4]], np.float32)
+    B = np.array([[1], [2]], np.float32)
+    wn, _, _ = _row_norm(dfx, W, A, B, 1.0, 2, 0)
+    assert np.allclose(wn, [5.0, 10.0], rtol=1e-6)
+    W = np.eye(4, dtype=np.float32)
+    A, B = oracle.seeded_gaussian(2, 4, 3), oracle.seeded_gaussian(4, 2, 4)
+    wn, _, _ = _row_norm(dfx, W, A, B, 0.0, 4, 0)
+    assert np.all(wn == 1.0)
+
+
+@pytest.mark.parametrize("dt", [0, 2])
+def test_acceptance_criterion1_grid(dfx, oracle, dt):
+    """acceptance.cpp:54-89: 300 instances, d_out/d_in in {3,17,64,96,257}, r in
+    {1,2,8,33}, s in {0, 1, 2/sqrt(r)}: GPU vs the oracle's own result and vs fp64."""
+    o = oracle
+    dims, ranks = [3, 17, 64, 96, 257], [1, 2, 8, 33]
+    seed = 10000
+    worst_ref = worst_f64 = 0.0
+    n = 0
+    for d_out in dims:
+        for d_in in dims:
+            for r in ranks:
+                for sm in range(3):
+                    s = 0.0 if sm == 0 else (1.0 if sm == 1 else 2.0 / np.sqrt(r))
+                    seed += 1
+                    W, A, B = _fixture(o, d_out, d_in, r, seed, dt)
+                    cs, _ = o.plan_chunks(d_out, d_in)
+                    got, _, _ = _row_norm(dfx, W, A, B, s, cs, dt)
+                    want = o.row_norm(dt, W, A, B, s, cs)
+                    f64 = o.dense_row_norm_f64(W, A, B, s)
+                    kap = _kappa(o, W, A, B, s)
+                    rel_ref = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
+                    rel_64 = np.abs(got - f64) / np.maximum(np.abs(f64), 1e-30)
+                    tol = 1e-5 if dt == 0 else 2e-3
+                    bound = np.maximum(tol, 64 * kap * 2.0 ** -24)
+                    assert np.all(rel_64 <= bound), (d_out, d_in, r, s, rel_64.max())
+                    assert np.all(rel_ref <= 2 * bound), (d_out, d_in, r, s, rel_ref.max())
+                    if s == 0.0:
+                        assert bits_equal(got, want)  # serial chain + sqrt, bitwise
+                    worst_ref = max(worst_ref, rel_ref.max())
+                    worst_f64 = max(worst_f64, rel_64.max())
+                    n += 1
+    assert n == 300
+    print(f"criterion 1 ({'fp32' if dt == 0 else 'fp16'}): {n} instances, max rel err vs "
+          f"reference {worst_ref:.2e}, vs fp64 {worst_f64:.2e}")
+
+
+@pytest.mark.parametrize("d_out,d_in,r,cs", [(24, 80, 1, 80), (24, 80, 768, 80), (64, 257, 4, 64),
+                                             (300, 1000, 12, 128), (129, 4096, 8, 4096)])
+def test_base_sq_bitwise_fp32(dfx, oracle, d_out, d_in, r, cs):
+    """base_sq is the reference's serial chunked chain, bitwise (factored_norm.cpp:52-61)."""
+    W, A, B = _fixture(oracle, d_out, d_in, r, d_out + d_in + r)
+    want = oracle.norm_terms(W, A, B, 1.0, cs)
+    got = _terms(dfx, W, A, B, 1.0, cs, 0)
+    assert bits_equal(got[0], want[0])
+    np.testing.assert_allclose(got[1], want[1], rtol=1e-4, atol=1e-3 * np.abs(want[1]).max())
+    np.testing.assert_allclose(got[2], want[2], rtol=1e-4, atol=1e-4 * np.abs(want[2]).max())
+
+
+@pytest.mark.parametrize("d_out,d_in,r", [(256, 512, 64), (1024, 1024, 384), (300, 640, 40),
+                                          (128, 4096, 512), (1000, 2048, 128), (8192, 256, 16),
+                                          (512, 8192, 1024)])
+def test_bf16_tensor_core_path(dfx, oracle, d_out, d_in, r):
+    """tcgen05/TMA path: base_sq bitwise; cross/ba_sq vs the oracle's fp32 terms; the
+    dtype-rounded norm within one bf16 ulp of the reference's and 1e-2 of fp64."""
+    assert dfx.uses_tensor_cores(1, d_out, d_in, r)
+    W, A, B = _fixture(oracle, d_out, d_in, r, 31 * d_out + r, dt=1)
+    s = 2.0 / np.sqrt(r)
+    cs, _ = oracle.plan_chunks(d_out, d_in)
+    want = oracle.norm_terms(W, A, B, s, cs)
+    m = np.abs(oracle.gaussian_vector(d_out, 1.0, 0.1, 5))
+    wn, g, t = _row_norm(dfx, W, A, B, s, cs, 1, m=m)
+    assert bits_equal(t[0], want[0])
+    scale_c = np.sqrt(want[0] * np.abs(want[2])) + 1e-30       # Cauchy-Schwarz size of cross
+    assert np.all(np.abs(t[1] - want[1]) <= 2e-5 * scale_c + 1e-6 * np.abs(want[1]))
+    assert np.all(np.abs(t[2] - want[2]) <= 1e-4 * np.abs(want[2]) + 1e-6 * want[2].max())
+    want_n = oracle.row_norm(1, W, A, B, s, cs)
+    ulp = np.spacing(want_n.astype(np.float32)) * 2 ** 16     # bf16 ulp at each value
+    assert np.all(np.abs(wn - want_n) <= ulp)
+    want_g = oracle.magnitude_scale(1, m, wn)                  # g given OUR norm: bitwise
+    assert bits_equal(g, want_g)
+    if d_out * d_in * r <= 2 ** 28:
+        f64 = oracle.dense_row_norm_f64(W, A, B, s)
+        assert np.max(np.abs(wn - f64) / f64) <= 1e-2
+
+
+def test_full_size_c2_sampled_rows(dfx, oracle):
+    """BASELINE C2 (8192^2, r=384, bf16) at full size: every row's base_sq bitwise vs the
+    serial chain, and 256 sampled rows' terms vs the oracle run on those rows."""
+    import torch
+    d_out = d_in = 8192
+    r = 384
+    rng = np.random.default_rng(20261017)
+    W = to_np(to_dev(rng.standard_normal((d_out, d_in), dtype=np.float32), 1))
+    A = to_np(to_dev(rng.standard_normal((r, d_in), dtype=np.float32), 1))
+    B = to_np(to_dev(rng.standard_normal((d_out, r), dtype=np.float32), 1))
+    s = 2.0 / np.sqrt(r)
+    cs, nc = oracle.plan_chunks(d_out, d_in)
+    assert nc == 1
+    t = np.stack(_terms(dfx, W, A, B, s, cs, 1))
+    base_want = oracle.norm_terms(W, A, B, 0.0, cs)[0]          # s = 0: chain only
+    assert bits_equal(t[0], base_want)
+    rows = np.sort(rng.choice(d_out, 256, replace=False))
+    sub = oracle.norm_terms(np.ascontiguousarray(W[rows]), A, np.ascontiguousarray(B[rows]), s, cs)
+    scale_c = np.sqrt(sub[0] * sub[2])
+    assert np.all(np.abs(t[1][rows] - sub[1]) <= 2e-5 * scale_c)
+    assert np.all(np.abs(t[2][rows] - sub[2]) <= 1e-4 * sub[2])
+    torch.cuda.synchronize()
+
+
+def test_assemble_and_magnitude_bitwise(dfx, oracle):
+    """assemble_norm (factored_norm.cpp:122-136) and magnitude_scale (:219-240) bitwise,
+    including clamp, NaN, -0, eps floor and bf16/fp16 rounding."""
+    import torch
+    rng = np.random.default_rng(3)
+    n = 4099
+    base = np.abs(rng.standard_normal(n).astype(np.float32)) * 100
+    cross = rng.standard_normal(n).astype(np.float32) * 50
+    ba = np.abs(rng.standard_normal(n).astype(np.float32)) * 30
+    base[:6] = [0.0, -0.0, np.nan, 1.0, 0.0, np.inf]
+    cross[:6] = [-1.0, 0.0, 0.0, 0.0, 0.0, -np.inf]
+    for two_s, s2 in [(2.0, 1.0), (2 * 0.1020620726159658, 0.1020620726159658 ** 2), (0.0, 0.0)]:
+        want = oracle.assemble(base, cross, ba, two_s, s2)
+        dev = [torch.from_numpy(x).cuda() for x in (base, cross, ba)]
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+        dfx.assemble(dev[0], dev[1], dev[2], two_s, s2, out)
+        torch.cuda.synchronize()
+        assert bits_equal(out.cpu().numpy(), want)
+    for dt in (0, 1, 2):
+        wn = np.array([oracle.round_to_dtype(v, dt) for v in
+                       np.concatenate([[0.0, np.nan, 1e-13, 1e-7, 3.0], np.abs(rng.standard_normal(500))])],
+                      np.float32)
+        m = rng.standard_normal(wn.shape[0]) * 2
+        want = oracle.magnitude_scale(dt, m, wn)
+        md = torch.from_numpy(m.astype(np.float32)).cuda()
+        g = torch.empty(wn.shape[0], dtype=torch.float32, device="cuda")
+        dfx.magnitude_scale(dt, md, torch.from_numpy(wn).cuda(), g)
+        torch.cuda.synchronize()
+        assert bits_equal(g.cpu().numpy(), want)
+
+
+def test_golden_norm(dfx):
+    """Terms and norms produced by the reference itself (tests/golden/norm.npz)."""
+    z = np.load(os.path.join(GOLDEN, "norm.npz"))
+    for k in range(int(z["n_cases"])):
+        dt, s, cs = int(z[f"n{k}_dt"]), float(z[f"n{k}_s"]), int(z[f"n{k}_cs"])
+        W, A, B = z[f"n{k}_W"], z[f"n{k}_A"], z[f"n{k}_B"]
+        t = _terms(dfx, W, A, B, s, cs, dt)
+        assert bits_equal(t[0], z[f"n{k}_base"]), k
+        wn, _, _ = _row_norm(dfx, W, A, B, s, cs, dt)
+        want = z[f"n{k}_norm"]
+        f64 = z[f"n{k}_f64"]
+        kap = z[f"n{k}_kappa"]
+        tol = 1e-5 if dt == 0 else 1e-2
+        bound = np.maximum(tol, 64 * kap * 2.0 ** -24)
+        assert np.all(np.abs(wn - f64) / np.maximum(f64, 1e-30) <= bound), k
+        assert np.all(np.abs(wn - want) / np.maximum(want, 1e-30) <= 2 * bound), k
+
+
+def test_invalid_arguments(dfx):
+    import torch
+    import paper_2603_22276_b200 as P
+    w = torch.zeros(8, 16, device="cuda")
+    a = torch.zeros(2, 16, device="cuda")
+    b = torch.zeros(8, 2, device="cuda")
+    o = torch.empty(8, device="cuda")
+    with pytest.raises(P.DfxInvalidArgument):
+        dfx.norm_terms(w, a[:0], b, 1.0, 16, o, o, o)       # rank 0
+    with pytest.raises(P.DfxInvalidArgument):
+        dfx.norm_terms(w, a, b, 1.0, 0, o, o, o)            # bad chunk plan

@@ -323,7 +323,8 @@ int dfx_compose_bwd(dfx_ctx* ctx, dfx_dtype dtype, const void* dy, const float* 
     if (rc) return rc;
     if (!valid_dtype(dtype)) return fail(DFX_EUNSUPPORTED, "compose_backward: dtype");
     if (rows < 0 || d_out < 0) return fail(DFX_EINVAL, "compose_backward: g length != d_out");
-    if (d_mag && !inner)
+    // an empty inner (rows == 0) may legitimately have a null data pointer
+    if (d_mag && !inner && rows > 0)
         return fail(DFX_EINVAL, "compose_backward: magnitude gradient requires inner");
     if (d_mag && !w_norm) return fail(DFX_EINVAL, "compose_backward: w_norm length != d_out");
     if (rows > 0 && d_out > 0 && (!dy || !g || !d_lora || !d_base))

@@ -290,7 +290,8 @@ int norm_uses_tensor_cores(int dt, int64_t d_out, int64_t d_in, int64_t r) {
 
 cudaError_t launch_norm(const NormArgs& a, Workspace* ws, cudaStream_t st, int* launches) {
     if (a.d_out == 0) return cudaSuccess;
-    if (a.s != 0.0 && norm_tc_supported(a.dt, a.d_out, a.d_in, a.r))
+    // the tensor-core chain walks 64-wide K blocks: chunk boundaries must align to them
+    if (a.s != 0.0 && a.chunk_size % 64 == 0 && norm_tc_supported(a.dt, a.d_out, a.d_in, a.r))
         return launch_norm_tc(a, ws, st, launches);
     switch (a.dt) {
         case kF32: return norm_simt_impl<float>(a, ws, st, launches);

@@ -46,7 +46,7 @@ struct TcParams {
     // rowdot
     const __nv_bfloat16* Z; int64_t ldz;
     float* out;             // rowdot: [k_split*n_split][M]; store: tiles
-    float* base_out;        // chain: [k_split][M]
+    float* base_out;        // chain: [num_chunks][M], one serial partial per chunk
     int do_chain;
     // store (gram): tile index mapping
     int gram_nt;            // tiles per side
@@ -171,14 +171,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = q * 32 + lane;        // row inside the tile
         const int64_t gm = m0 + row;
         if (chain) {
-            float partial = 0.0f, base = 0.0f;
+            // one serial fp32 partial per ChunkPlan chunk (factored_norm.cpp:52-60); the
+            // finisher adds the chunk partials in ascending order (:60), so K splits on
+            // chunk boundaries keep base_sq bitwise equal to the reference
+            float partial = 0.0f;
+            int64_t cur = -1;
             for (int it = 0; it < nkb; ++it) {
                 const int s = it % p.stages;
                 mbar_wait(&full[s], (it / p.stages) & 1);
-                const int64_t gk0 = int64_t(kb0 + it) * kBK;
-                if (gk0 > 0 && gk0 % p.chunk == 0 && it > 0) {
-                    base = __fadd_rn(base, partial);
+                const int64_t chunk_idx = (int64_t(kb0 + it) * kBK) / p.chunk;
+                if (chunk_idx != cur) {
+                    if (cur >= 0 && gm < p.M) p.base_out[cur * p.M + gm] = partial;
                     partial = 0.0f;
+                    cur = chunk_idx;
                 }
                 const uint8_t* rowp = smem + s * stage_bytes + row * 128;
 #pragma unroll
@@ -192,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
             }
-            if (gm < p.M) p.base_out[int64_t(ks) * p.M + gm] = __fadd_rn(base, partial);
+            if (cur >= 0 && gm < p.M) p.base_out[cur * p.M + gm] = partial;
         }
         // wait for the accumulator
         if (nkb > 0) {
@@ -320,7 +325,7 @@ cudaError_t launch_tc(int mode, const CUtensorMap& tx, const CUtensorMap& ty, Tc
 // row in one CTA, bitwise) and uses K splits only when N splitting cannot fill.
 struct Split { int ns, ks, bn; };
 
-Split choose_split(int64_t m_tiles, int64_t r, int64_t kb_total, bool allow_k) {
+Split choose_split(int64_t m_tiles, int64_t r, int64_t kb_total, int max_ks) {
     const int kSMs = 148;
     Split best{1, 1, 0};
     double best_score = -1.0;
@@ -329,7 +334,7 @@ Split choose_split(int64_t m_tiles, int64_t r, int64_t kb_total, bool allow_k) {
         const int bn = static_cast<int>(((r + ns - 1) / ns + 15) / 16 * 16);
         if (bn > 256 || bn < 16) continue;
         if (ns > ns_min && bn < 64) break;
-        for (int ks = 1; ks <= (allow_k ? 8 : 1); ks *= 2) {
+        for (int ks = 1; ks <= max_ks && ks <= 8; ks *= 2) {
             if (ks > 1 && kb_total / ks < 4) break;
             const int64_t ctas = m_tiles * ns * ks;
             const int64_t waves = (ctas + kSMs - 1) / kSMs;
@@ -391,7 +396,7 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
 
     const int64_t m_tiles = (d_out + kBM - 1) / kBM;
     // ---------------- ba_sq partials: rowdot(B [G_hi|G_lo], B) ----------------
-    const Split sb = choose_split(m_tiles, r, 2 * r_pad / kBK, false);
+    const Split sb = choose_split(m_tiles, r, 2 * r_pad / kBK, 1);
     float* ba = static_cast<float*>(ws_get(ws, kWsBa, size_t(sb.ns) * d_out * sizeof(float), &err));
     if (err != cudaSuccess) return err;
     {
@@ -413,13 +418,18 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
     }
 
     // ---------------- cross partials + base_sq chain: rowdot(W A^T, B) ----------------
-    const Split su = choose_split(m_tiles, r, kb_in, true);
-    const int kbps = static_cast<int>((kb_in + su.ks - 1) / su.ks);
+    // K splits only on ChunkPlan boundaries (each split = whole chunks)
+    const int64_t chunk_blocks = a.chunk_size / kBK;
+    const int64_t n_chunks = (d_in + a.chunk_size - 1) / a.chunk_size;
+    const Split su = choose_split(m_tiles, r, kb_in, static_cast<int>(std::min<int64_t>(n_chunks, 8)));
+    const int64_t chunks_per_split = (n_chunks + su.ks - 1) / su.ks;
+    const int kbps = static_cast<int>(chunks_per_split * chunk_blocks);
     const int ks = static_cast<int>((kb_in + kbps - 1) / kbps);
     float* cross = static_cast<float*>(
         ws_get(ws, kWsCross, size_t(ks) * su.ns * d_out * sizeof(float), &err));
     if (err != cudaSuccess) return err;
-    float* base = static_cast<float*>(ws_get(ws, kWsBase, size_t(ks) * d_out * sizeof(float), &err));
+    float* base = static_cast<float*>(
+        ws_get(ws, kWsBase, size_t(n_chunks) * d_out * sizeof(float), &err));
     if (err != cudaSuccess) return err;
     {
         CUtensorMap tw, ta;
@@ -440,7 +450,7 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
     }
 
     FinishArgs f{};
-    f.base_part = base; f.base_parts = ks;
+    f.base_part = base; f.base_parts = static_cast<int>(n_chunks);
     f.cross_part = cross; f.cross_parts = ks * su.ns;
     f.ba_part = ba; f.ba_parts = sb.ns;
     f.d_out = d_out; f.two_s = 2.0 * a.s; f.s2 = a.s * a.s;

@@ -6,6 +6,7 @@
 // arithmetic contract, not against itself.
 //
 // Run on a B200: tests/cpp/test_dropin [filter]   (driven by tests/test_gpu_dropin.py)
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -220,11 +221,17 @@ TEST("norm: base_sq bitwise rank-independent, r=1 vs r=768 (test_factored_norm.c
     const NormTerms t1 = factored_norm_terms(w, make_adapter(d_out, d_in, 1, 1.0, 501), plan);
     const NormTerms t2 = factored_norm_terms(w, make_adapter(d_out, d_in, 768, 1.0, 502), plan);
     CHECK(std::memcmp(t1.base_sq.data(), t2.base_sq.data(), d_out * sizeof(float)) == 0);
-    // and equal to the serial chain itself
+    // and equal to the chunked serial chain itself (d_in=80 plans chunks of 64 + 16)
+    REQUIRE(plan.chunk_size == 64);
     for (index_t i = 0; i < d_out; ++i) {
-        float acc = 0.0f;
-        for (index_t k = 0; k < d_in; ++k) acc += static_cast<float>(w(i, k)) * static_cast<float>(w(i, k));
-        CHECK(t1.base_sq[i] == acc);
+        float base = 0.0f;
+        for (index_t c0 = 0; c0 < d_in; c0 += plan.chunk_size) {
+            float partial = 0.0f;
+            for (index_t k = c0; k < std::min(d_in, c0 + plan.chunk_size); ++k)
+                partial += static_cast<float>(w(i, k)) * static_cast<float>(w(i, k));
+            base += partial;
+        }
+        CHECK(t1.base_sq[i] == base);
     }
 }
 

@@ -65,6 +65,13 @@ void dfx_ctx_destroy(dfx_ctx* ctx);
 /* Number of kernels launched by this context since creation (evidence counter). */
 int64_t dfx_ctx_launches(const dfx_ctx* ctx);
 
+/* Per-kernel device timing.  While enabled, every kernel the context launches is
+ * bracketed by CUDA events on its stream.  dfx_profile_report synchronises the device,
+ * writes one line per kernel ("name launches total_ms min_ms max_ms\n") into buf and
+ * resets the records. */
+int dfx_profile_enable(dfx_ctx* ctx, int on);
+int dfx_profile_report(dfx_ctx* ctx, char* buf, size_t len);
+
 /* plan_chunks (matrix.hpp:68, matrix.cpp:28-51): host-only, no device needed.
  * DFX_EINVAL where the reference throws. */
 int dfx_plan_chunks(uint64_t d_out, uint64_t d_in, uint64_t budget_bytes,

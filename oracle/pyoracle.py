@@ -191,7 +191,13 @@ class Reference:
         L.ref_gaussian_vector.argtypes = [_sz, C.c_double, C.c_double, C.c_uint64, _dp]
         L.ref_derive_seed.restype = C.c_uint64
         L.ref_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.ref_last_call_ns.restype = C.c_int64
+        L.ref_last_call_ns.argtypes = []
         self.L = L
+
+    def last_call_s(self) -> float:
+        """Wall time of this thread's last reference call (RealMatrix packing excluded)."""
+        return self.L.ref_last_call_ns() * 1e-9
 
     def round_to_dtype(self, x, dtype):
         return self.L.ref_round_to_dtype(float(x), dtype)

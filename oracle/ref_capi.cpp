@@ -7,9 +7,11 @@
 // reference entry points; it adds no arithmetic of its own.  It is used to pin
 // oracle/oracle.c (tests/test_oracle.py), to generate tests/golden/, and as the
 // `--impl reference` CPU arm of bench.py.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <optional>
 #include <vector>
 
 #include "dorafactor/compose.hpp"
@@ -19,6 +21,18 @@
 namespace R = dorafactor;  // renamed to dorafactor_ref by the -D flag
 
 namespace {
+
+// wall time of the last reference call made by this thread, packing excluded
+thread_local std::int64_t g_last_ns = 0;
+
+struct CallTimer {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    ~CallTimer() {
+        g_last_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                        std::chrono::steady_clock::now() - t0)
+                        .count();
+    }
+};
 
 const R::DTypeSpec& spec(int dtype) {
     switch (dtype) {
@@ -44,6 +58,8 @@ void unpack(const R::RealMatrix& m, float* out) {
 }  // namespace
 
 extern "C" {
+
+std::int64_t ref_last_call_ns() { return g_last_ns; }
 
 int ref_plan_chunks(std::size_t d_out, std::size_t d_in, std::uint64_t budget,
                     std::size_t* chunk_size, std::size_t* num_chunks) {
@@ -88,7 +104,11 @@ int ref_row_norm(int dtype, const float* w, const float* a, const float* b, std:
         R::ChunkPlan plan;
         plan.chunk_size = chunk_size;
         plan.num_chunks = (d_in + chunk_size - 1) / chunk_size;
-        const std::vector<double> n = R::factored_row_norm(W, ad, plan);
+        std::vector<double> n;
+        {
+            CallTimer t;
+            n = R::factored_row_norm(W, ad, plan);
+        }
         std::memcpy(out, n.data(), d_out * sizeof(double));
         return 0;
     } catch (const std::exception&) {
@@ -130,17 +150,24 @@ int ref_compose(int variant, int dtype, const float* base, const float* lora, co
         const R::RealMatrix Lm = pack(lora, rows, d_out, dtype);
         const std::vector<double> gv(g, g + d_out);
         const R::ComposeInputs in{Bm, Lm, gv, s, spec(dtype)};
-        switch (variant) {
-            case 0: unpack(R::stable_compose(in), delta); break;
-            case 1: unpack(R::fused_compose(in).delta, delta); break;
-            case 2: {
-                const R::DualResult d = R::dual_output_compose(in, inner != nullptr);
-                unpack(d.delta, delta);
-                if (inner) unpack(*d.inner, inner);
-                break;
+        R::RealMatrix d;
+        std::optional<R::RealMatrix> inn;
+        {
+            CallTimer t;
+            switch (variant) {
+                case 0: d = R::stable_compose(in); break;
+                case 1: d = R::fused_compose(in).delta; break;
+                case 2: {
+                    R::DualResult r = R::dual_output_compose(in, inner != nullptr);
+                    d = std::move(r.delta);
+                    inn = std::move(r.inner);
+                    break;
+                }
+                default: d = R::naive_compose(in); break;
             }
-            default: unpack(R::naive_compose(in), delta); break;
         }
+        unpack(d, delta);
+        if (inner && inn) unpack(*inn, inner);
         return 0;
     } catch (const std::exception&) {
         return -1;
@@ -157,8 +184,11 @@ int ref_compose_bwd(int dtype, const float* dy, const double* g, double s, const
         const std::vector<double> gv(g, g + d_out);
         const std::vector<double> wn =
             w_norm ? std::vector<double>(w_norm, w_norm + d_out) : std::vector<double>();
-        const R::GradBundle gb =
-            R::compose_backward(D, gv, s, inner ? &I : nullptr, wn, mag_grad != 0);
+        R::GradBundle gb{R::RealMatrix(), R::RealMatrix(), std::nullopt};
+        {
+            CallTimer t;
+            gb = R::compose_backward(D, gv, s, inner ? &I : nullptr, wn, mag_grad != 0);
+        }
         unpack(gb.d_lora, d_lora);
         unpack(gb.d_base, d_base);
         if (mag_grad && d_mag) std::memcpy(d_mag, gb.d_mag->data(), d_out * sizeof(double));

@@ -57,6 +57,8 @@ SIGNATURES = {
     "dfx_ctx_create": (_int, [_int, C.POINTER(_vp)]),
     "dfx_ctx_destroy": (None, [_vp]),
     "dfx_ctx_launches": (_i64, [_vp]),
+    "dfx_profile_enable": (_int, [_vp, _int]),
+    "dfx_profile_report": (_int, [_vp, C.c_char_p, C.c_size_t]),
     "dfx_plan_chunks": (_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64),
                                C.POINTER(C.c_uint64)]),
     "dfx_norm_terms": (_int, [_vp, _int, _vp, _vp, _vp, _i64, _i64, _i64, _f64, _i64,
@@ -202,6 +204,20 @@ class Dfx:
                                                  _ptr(m), _ptr(base), _ptr(lora), float(s),
                                                  d_out, d_in, r, rows, chunk_size, _ptr(delta),
                                                  _ptr(g)))
+
+    # ------------------------------------------------------------ profiling
+    def profile(self, on: bool = True):
+        self._check(self.lib.dfx_profile_enable(self.ctx, int(on)))
+
+    def profile_report(self) -> dict:
+        """{kernel: (launches, total_ms, min_ms, max_ms)}; synchronises and resets."""
+        buf = C.create_string_buffer(1 << 16)
+        self._check(self.lib.dfx_profile_report(self.ctx, buf, len(buf)))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, n, tot, mn, mx = line.split()
+            out[name] = (int(n), float(tot), float(mn), float(mx))
+        return out
 
     # ----------------------------------------------------------------- misc
     def plan_chunks(self, d_out, d_in, budget=268435456):

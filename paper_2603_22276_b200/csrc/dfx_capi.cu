@@ -11,6 +11,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -23,14 +24,39 @@ namespace dfx {
 
 struct Workspace {
     int device = 0;
+    int sms = 0;
     std::vector<void*> ptr;
     std::vector<size_t> cap;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     Workspace() : ptr(16, nullptr), cap(16, 0) {}
     ~Workspace() {
         for (void* p : ptr)
             if (p) cudaFree(p);
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
+        if (side) cudaStreamDestroy(side);
     }
 };
+
+cudaStream_t ws_side_stream(Workspace* ws, cudaError_t* err) {
+    *err = cudaSuccess;
+    if (!ws->side) *err = cudaStreamCreateWithFlags(&ws->side, cudaStreamNonBlocking);
+    return ws->side;
+}
+
+cudaEvent_t ws_event(Workspace* ws, int idx, cudaError_t* err) {
+    if (!ws->ev[idx]) {
+        const cudaError_t e = cudaEventCreateWithFlags(&ws->ev[idx], cudaEventDisableTiming);
+        if (e != cudaSuccess) *err = e;
+    }
+    return ws->ev[idx];
+}
+
+int ws_sm_count(Workspace* ws) {
+    if (!ws->sms) cudaDeviceGetAttribute(&ws->sms, cudaDevAttrMultiProcessorCount, ws->device);
+    return ws->sms > 0 ? ws->sms : 148;
+}
 
 void* ws_get(Workspace* ws, int slot, size_t bytes, cudaError_t* err) {
     *err = cudaSuccess;
@@ -91,12 +117,60 @@ cudaError_t make_tmap_2d(CUtensorMap* out, int dt, const void* base, uint64_t ro
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// ----------------------------------------------------------------- profiling
+struct Profiler {
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    const char* open_name = nullptr;
+    cudaEvent_t open_ev = nullptr;
+    cudaEvent_t take() {
+        cudaEvent_t e;
+        if (!pool.empty()) {
+            e = pool.back();
+            pool.pop_back();
+        } else {
+            cudaEventCreate(&e);
+        }
+        return e;
+    }
+    ~Profiler() {
+        for (auto& r : recs) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
+thread_local Profiler* g_prof = nullptr;
+
+void prof_begin(const char* name, cudaStream_t st) {
+    if (!g_prof) return;
+    g_prof->open_name = name;
+    g_prof->open_ev = g_prof->take();
+    cudaEventRecord(g_prof->open_ev, st);
+}
+
+void prof_end(cudaStream_t st) {
+    if (!g_prof || !g_prof->open_ev) return;
+    cudaEvent_t b = g_prof->take();
+    cudaEventRecord(b, st);
+    g_prof->recs.push_back({g_prof->open_name, g_prof->open_ev, b});
+    g_prof->open_ev = nullptr;
+}
+
 }  // namespace dfx
 
 struct dfx_ctx {
     int device = 0;
     dfx::Workspace ws;
     int64_t launches = 0;
+    bool profiling = false;
+    dfx::Profiler prof;
     // module_fwd_host staging
     cudaStream_t st_h2d = nullptr, st_comp = nullptr, st_d2h = nullptr;
     std::vector<void*> stage;
@@ -123,11 +197,12 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 bool valid_dtype(int dt) { return dt == DFX_F32 || dt == DFX_BF16 || dt == DFX_F16; }
 
-// Binds the calling thread to the context's device.
+// Binds the calling thread to the context's device (and its profiler, if enabled).
 int enter(dfx_ctx* ctx) {
     if (!ctx) return fail(DFX_EINVAL, "null context");
     const cudaError_t e = cudaSetDevice(ctx->device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    dfx::g_prof = ctx->profiling ? &ctx->prof : nullptr;
     return DFX_OK;
 }
 
@@ -185,6 +260,59 @@ void dfx_ctx_destroy(dfx_ctx* ctx) {
 }
 
 int64_t dfx_ctx_launches(const dfx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int dfx_profile_enable(dfx_ctx* ctx, int on) {
+    if (!ctx) return fail(DFX_EINVAL, "null context");
+    ctx->profiling = on != 0;
+    if (!ctx->profiling) dfx::g_prof = nullptr;
+    g_err.clear();
+    return DFX_OK;
+}
+
+int dfx_profile_report(dfx_ctx* ctx, char* buf, size_t len) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "dfx_profile_report");
+    struct Agg {
+        std::string name;
+        long n = 0;
+        double tot = 0, mn = 1e30, mx = 0;
+    };
+    std::vector<Agg> agg;
+    dfx::Profiler& P = ctx->prof;
+    for (auto& r : P.recs) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        Agg* a = nullptr;
+        for (auto& x : agg)
+            if (x.name == r.name) a = &x;
+        if (!a) {
+            agg.push_back(Agg{r.name});
+            a = &agg.back();
+        }
+        ++a->n;
+        a->tot += ms;
+        a->mn = std::min<double>(a->mn, ms);
+        a->mx = std::max<double>(a->mx, ms);
+        P.pool.push_back(r.a);
+        P.pool.push_back(r.b);
+    }
+    P.recs.clear();
+    std::string out;
+    for (auto& a : agg) {
+        char line[256];
+        std::snprintf(line, sizeof(line), "%s %ld %.6f %.6f %.6f\n", a.name.c_str(), a.n, a.tot,
+                      a.mn, a.mx);
+        out += line;
+    }
+    if (buf && len) {
+        std::snprintf(buf, len, "%s", out.c_str());
+        if (out.size() + 1 > len) return fail(DFX_EINVAL, "dfx_profile_report: buffer too small");
+    }
+    g_err.clear();
+    return DFX_OK;
+}
 
 int dfx_plan_chunks(uint64_t d_out, uint64_t d_in, uint64_t budget, uint64_t* chunk_size,
                     uint64_t* num_chunks) {

@@ -385,14 +385,18 @@ cudaError_t fwd_impl(const void* base, const void* lora, const float* g, float s
         const int by = 256 / bx;
         const int64_t gx = (cv + bx - 1) / bx;
         const int64_t gy = std::min<int64_t>((rows + by * R - 1) / (by * R), 65535);
+        prof_begin(kInner ? "compose_fwd_dual" : "compose_fwd", st);
         compose_fwd_vec<T, kInner, R>
             <<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)), dim3(bx, by), 0, st>>>(
                 b, l, g, sf, rows, d_out, d, in);
+        prof_end(st);
     } else {
         const int64_t n = rows * d_out;
         const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+        prof_begin("compose_fwd_generic", st);
         compose_fwd_generic<T, kInner><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
             b, l, g, sf, rows, d_out, d, in);
+        prof_end(st);
     }
     return cudaGetLastError();
 }
@@ -416,12 +420,16 @@ cudaError_t bwd_impl(int dt, const void* dy, const float* g, float sf, const voi
             const int by = 256 / bx;
             const int64_t gx = (cv + bx - 1) / bx;
             const int64_t gy = std::min<int64_t>((rows + by * R - 1) / (by * R), 65535);
+            prof_begin("compose_bwd", st);
             compose_bwd_vec<T, R><<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)),
                                     dim3(bx, by), 0, st>>>(y, g, sf, rows, d_out, dl, db);
+            prof_end(st);
         } else {
+            prof_begin("compose_bwd_generic", st);
             compose_bwd_generic<T, false>
                 <<<static_cast<unsigned>((d_out + 127) / 128), 128, 0, st>>>(
                     y, g, sf, nullptr, nullptr, rows, d_out, dl, db, nullptr);
+            prof_end(st);
         }
         return cudaGetLastError();
     }
@@ -442,11 +450,15 @@ cudaError_t bwd_impl(int dt, const void* dy, const float* g, float sf, const voi
             attr_set = true;
         }
         const unsigned grid = static_cast<unsigned>((d_out + C::kSC - 1) / C::kSC);
+        prof_begin("compose_bwd_dmag", st);
         compose_bwd_serial<T><<<grid, C::kThreads, C::kSmem, st>>>(
             tm_dy, tm_in, g, sf, w_norm, rows, d_out, dl, db, d_mag);
+        prof_end(st);
     } else {
+        prof_begin("compose_bwd_dmag_generic", st);
         compose_bwd_generic<T, true><<<static_cast<unsigned>((d_out + 127) / 128), 128, 0, st>>>(
             y, g, sf, in, w_norm, rows, d_out, dl, db, d_mag);
+        prof_end(st);
     }
     return cudaGetLastError();
 }

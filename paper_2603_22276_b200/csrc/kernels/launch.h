@@ -48,8 +48,18 @@ struct NormArgs {
     int mag_dt;       // working dtype of the magnitude division
 };
 
+// Per-launch device timing (dfx_profile_enable): launch sites bracket each kernel
+// with these; they are no-ops unless the calling thread is inside a call on a
+// profiling context.
+void prof_begin(const char* name, cudaStream_t st);
+void prof_end(cudaStream_t st);
+
 struct Workspace;  // owned by the context (dfx_capi.cu)
 void* ws_get(Workspace* ws, int slot, size_t bytes, cudaError_t* err);
+// Context-owned side stream (non-blocking) and fork/join events for intra-call concurrency.
+cudaStream_t ws_side_stream(Workspace* ws, cudaError_t* err);
+cudaEvent_t ws_event(Workspace* ws, int idx, cudaError_t* err);
+int ws_sm_count(Workspace* ws);
 
 cudaError_t launch_norm(const NormArgs& a, Workspace* ws, cudaStream_t st, int* launches);
 

@@ -222,7 +222,9 @@ cudaError_t norm_simt_impl(const NormArgs& a, Workspace* ws, cudaStream_t st, in
     f.base_part = base; f.base_parts = 1;
 
     if (a.s == 0.0) {
+        prof_begin("base_chain", st);
         base_chain<T><<<blocks_for(a.d_out, 32), 256, 0, st>>>(W, a.d_out, a.d_in, a.chunk_size, base);
+        prof_end(st);
         if (launches) ++*launches;
     } else {
         const int64_t nt = (a.r + kBN - 1) / kBN;
@@ -233,18 +235,24 @@ cudaError_t norm_simt_impl(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         float* ba = static_cast<float*>(ws_get(ws, kWsBa, nt * a.d_out * sizeof(float), &err));
         if (err != cudaSuccess) return err;
         // G = A A^T
+        prof_begin("simt_gram", st);
         simt_gemm<T, T, kStore, false>
             <<<dim3(blocks_for(a.r, kBM), static_cast<unsigned>(nt)), 256, 0, st>>>(
                 A, a.d_in, A, a.d_in, nullptr, 0, a.r, a.r, a.d_in, a.chunk_size, G, nullptr);
+        prof_end(st);
         // ba_sq partials: rowdot(B G, B); G is exactly symmetric (p,q and q,p use the
         // same products in the same order), so Y = G serves as (G^T)
+        prof_begin("simt_ba_rowdot", st);
         simt_gemm<T, float, kRowdot, false>
             <<<dim3(blocks_for(a.d_out, kBM), static_cast<unsigned>(nt)), 256, 0, st>>>(
                 B, a.r, G, a.r, B, a.r, a.d_out, a.r, a.r, a.chunk_size, ba, nullptr);
+        prof_end(st);
         // cross partials + base_sq chain: rowdot(W A^T, B)
+        prof_begin("simt_u_rowdot", st);
         simt_gemm<T, T, kRowdot, true>
             <<<dim3(blocks_for(a.d_out, kBM), static_cast<unsigned>(nt)), 256, 0, st>>>(
                 W, a.d_in, A, a.d_in, B, a.r, a.d_out, a.r, a.d_in, a.chunk_size, cross, base);
+        prof_end(st);
         if (launches) *launches += 3;
         f.cross_part = cross; f.cross_parts = static_cast<int>(nt);
         f.ba_part = ba; f.ba_parts = static_cast<int>(nt);
@@ -259,7 +267,9 @@ cudaError_t norm_simt_impl(const NormArgs& a, Workspace* ws, cudaStream_t st, in
 
 cudaError_t launch_finish(const FinishArgs& f, cudaStream_t st) {
     if (f.d_out <= 0) return cudaSuccess;
+    prof_begin("finish", st);
     finish_kernel<<<blocks_for(f.d_out, 256), 256, 0, st>>>(f);
+    prof_end(st);
     return cudaGetLastError();
 }
 
@@ -279,7 +289,9 @@ cudaError_t launch_assemble(const float* base_sq, const float* cross, const floa
 cudaError_t launch_magnitude_scale(int dt, const float* m, const float* w_norm, int64_t n,
                                    float* g, cudaStream_t st, int* launches) {
     if (n <= 0) return cudaSuccess;
+    prof_begin("magnitude", st);
     magnitude_kernel<<<blocks_for(n, 256), 256, 0, st>>>(m, w_norm, n, dt, g);
+    prof_end(st);
     if (launches) ++*launches;
     return cudaGetLastError();
 }

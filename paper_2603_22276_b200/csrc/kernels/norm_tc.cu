@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "norm_common.cuh"
 
@@ -50,6 +51,7 @@ struct TcParams {
     int do_chain;
     // store (gram): tile index mapping
     int gram_nt;            // tiles per side
+    int tiles;              // tiles per K split (the persistent loop's extent)
 };
 
 __device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
@@ -61,6 +63,24 @@ __device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
     }
 }
 
+// Tile t of split z (blockIdx.y): rowdot -> (m, n) = (t / n_split, t % n_split), adjacent
+// tiles share the X (W) rows; store (Gram) -> the t-th upper-triangle tile (pi <= qi).
+__device__ __forceinline__ void tile_coords(int kMode, const TcParams& p, int t, int64_t& m0,
+                                            int64_t& n0) {
+    if (kMode == kTcStore) {
+        int pi = 0;
+        while (t >= p.gram_nt - pi) { t -= p.gram_nt - pi; ++pi; }
+        m0 = int64_t(pi) * kBM;
+        n0 = int64_t(pi + t) * p.bn;
+    } else {
+        m0 = int64_t(t / p.n_split) * kBM;
+        n0 = int64_t(t % p.n_split) * p.bn;
+    }
+}
+
+// Persistent: CTA b walks tiles b, b + gridDim.x, ...; the smem stage ring and its
+// phases run on across tiles, and the TMEM accumulator is double-buffered (2 x BN
+// columns) so the MMA of tile i+1 overlaps the epilogue of tile i.
 template <int kMode>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_rowdot(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
@@ -72,45 +92,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int stage_bytes = kXStage + y_stage;  // both multiples of 1024
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
     uint64_t* empty = full + p.stages;
-    uint64_t* tmem_full = empty + p.stages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* tmem_full = empty + p.stages;     // [2]
+    uint64_t* tmem_empty = tmem_full + 2;       // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
     const int warp = warp_id(), lane = lane_id();
-
-    // ---- tile coordinates
-    int64_t m0, n0;
-    int ks;
-    if (kMode == kTcStore) {
-        // blockIdx.x enumerates upper-triangle tiles (pi <= qi), blockIdx.y the K split
-        int t = blockIdx.x, pi = 0;
-        while (t >= p.gram_nt - pi) { t -= p.gram_nt - pi; ++pi; }
-        const int qi = pi + t;
-        m0 = int64_t(pi) * kBM;
-        n0 = int64_t(qi) * p.bn;
-        ks = blockIdx.y;
-    } else {
-        const int ns = blockIdx.x % p.n_split;
-        m0 = int64_t(blockIdx.x / p.n_split) * kBM;
-        n0 = int64_t(ns) * p.bn;
-        ks = blockIdx.y;
-    }
-    const bool chain = (kMode == kTcRowdot) && p.do_chain && (n0 == 0);
+    const int ks = blockIdx.y;
     const int kb0 = ks * p.kb_per_split;
     const int64_t total_kb = (p.k_total + kBK - 1) / kBK;
     const int64_t kb_left = total_kb - kb0;
     const int nkb = static_cast<int>(kb_left < p.kb_per_split ? kb_left : p.kb_per_split);
+    const bool do_chain = (kMode == kTcRowdot) && p.do_chain;
 
+    // two accumulator slots, each starting on a 32-column boundary
+    const uint32_t slot_cols = static_cast<uint32_t>((p.bn + 31) / 32 * 32);
     uint32_t tmem_cols = 32;
-    while (tmem_cols < static_cast<uint32_t>(p.bn)) tmem_cols <<= 1;
+    while (tmem_cols < 2 * slot_cols) tmem_cols <<= 1;
 
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmx);
         tma_prefetch_desc(&tmy);
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1 + (chain ? 4 : 0));
+            mbar_init(&empty[s], 1 + (do_chain ? 4 : 0));
         }
-        mbar_init(tmem_full, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tmem_full[a], 1);
+            mbar_init(&tmem_empty[a], 4);
+        }
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -127,121 +136,173 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
+    if (nkb > 0 && warp == 0) {
         // ================= TMA producer =================
-        if (lane == 0 && nkb > 0) {
-            const uint64_t pol_x = (kMode == kTcRowdot && !p.x_kwrap) ? policy_evict_first()
-                                                                       : policy_evict_last();
+        if (lane == 0) {
+            const uint64_t pol_x = (kMode == kTcRowdot && !p.x_kwrap && p.n_split == 1)
+                                       ? policy_evict_first()
+                                       : policy_evict_last();
             const uint64_t pol_y = policy_evict_last();
-            for (int it = 0; it < nkb; ++it) {
-                const int s = it % p.stages;
-                mbar_wait(&empty[s], ((it / p.stages) & 1) ^ 1);
-                mbar_arrive_expect_tx(&full[s], stage_bytes);
-                uint8_t* sx = smem + s * stage_bytes;
-                uint8_t* sy = sx + kXStage;
-                const int kc = (kb0 + it) * kBK;
-                const int kx = p.x_kwrap ? kc % p.x_kwrap : kc;
-                tma_load_2d(&tmx, &full[s], sx, kx, static_cast<int32_t>(m0), pol_x);
-                tma_load_2d(&tmy, &full[s], sy, kc, static_cast<int32_t>(n0), pol_y);
-            }
-        }
-    } else if (warp == 1) {
-        // ================= MMA issuer (single thread) =================
-        if (lane == 0 && nkb > 0) {
-            const uint32_t idesc = umma_idesc_f16(1u, kBM, static_cast<uint32_t>(p.bn));
-            for (int it = 0; it < nkb; ++it) {
-                const int s = it % p.stages;
-                mbar_wait(&full[s], (it / p.stages) & 1);
-                tc_fence_after();
-                const uint32_t sx = smem_u32(smem + s * stage_bytes);
-                const uint32_t sy = sx + kXStage;
-#pragma unroll
-                for (int k = 0; k < kBK / 16; ++k) {
-                    const uint64_t ad = umma_desc_k_sw128(sx + k * 32);
-                    const uint64_t bd = umma_desc_k_sw128(sy + k * 32);
-                    umma_f16(tmem_base, ad, bd, idesc, (it > 0 || k > 0) ? 1u : 0u);
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+                int64_t m0, n0;
+                tile_coords(kMode, p, t, m0, n0);
+                for (int it = 0; it < nkb; ++it) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_arrive_expect_tx(&full[s], stage_bytes);
+                    uint8_t* sx = smem + s * stage_bytes;
+                    uint8_t* sy = sx + kXStage;
+                    const int kc = (kb0 + it) * kBK;
+                    const int kx = (p.x_kwrap && kc >= p.x_kwrap) ? kc - p.x_kwrap : kc;
+                    tma_load_2d(&tmx, &full[s], sx, kx, static_cast<int32_t>(m0), pol_x);
+                    tma_load_2d(&tmy, &full[s], sy, kc, static_cast<int32_t>(n0), pol_y);
+                    if (++s == p.stages) { s = 0; ph ^= 1; }
                 }
-                umma_commit(&empty[s]);
             }
-            umma_commit(tmem_full);
         }
-    } else if (warp >= 4) {
+    } else if (nkb > 0 && warp == 1) {
+        // ================= MMA issuer (single thread) =================
+        if (lane == 0) {
+            const uint32_t idesc = umma_idesc_f16(1u, kBM, static_cast<uint32_t>(p.bn));
+            int s = 0;
+            uint32_t ph = 0;
+            int local = 0;
+            for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++local) {
+                int64_t m0, n0;
+                tile_coords(kMode, p, t, m0, n0);
+                const bool tile_chain = do_chain && n0 == 0;
+                const int slot = local & 1;
+                const uint32_t tacc = tmem_base + static_cast<uint32_t>(slot) * slot_cols;
+                mbar_wait(&tmem_empty[slot], ((local >> 1) & 1) ^ 1);
+                tc_fence_after();
+                for (int it = 0; it < nkb; ++it) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t sx = smem_u32(smem + s * stage_bytes);
+                    const uint32_t sy = sx + kXStage;
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        const uint64_t ad = umma_desc_k_sw128(sx + k * 32);
+                        const uint64_t bd = umma_desc_k_sw128(sy + k * 32);
+                        umma_f16(tacc, ad, bd, idesc, (it > 0 || k > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&empty[s]);
+                    // tiles without a chain stand in for the 4 chain-warp arrivals
+                    if (do_chain && !tile_chain) mbar_arrive_cnt(&empty[s], 4);
+                    if (++s == p.stages) { s = 0; ph ^= 1; }
+                }
+                umma_commit(&tmem_full[slot]);
+            }
+        }
+    } else if (nkb > 0 && warp >= 4) {
         // ================= chain + epilogue (one row per thread) =================
         const int q = warp - 4;               // TMEM lane quadrant
         const int row = q * 32 + lane;        // row inside the tile
-        const int64_t gm = m0 + row;
-        if (chain) {
-            // one serial fp32 partial per ChunkPlan chunk (factored_norm.cpp:52-60); the
-            // finisher adds the chunk partials in ascending order (:60), so K splits on
-            // chunk boundaries keep base_sq bitwise equal to the reference
-            float partial = 0.0f;
-            int64_t cur = -1;
-            for (int it = 0; it < nkb; ++it) {
-                const int s = it % p.stages;
-                mbar_wait(&full[s], (it / p.stages) & 1);
-                const int64_t chunk_idx = (int64_t(kb0 + it) * kBK) / p.chunk;
-                if (chunk_idx != cur) {
-                    if (cur >= 0 && gm < p.M) p.base_out[cur * p.M + gm] = partial;
-                    partial = 0.0f;
-                    cur = chunk_idx;
-                }
-                const uint8_t* rowp = smem + s * stage_bytes + row * 128;
+        const uint32_t swz = static_cast<uint32_t>(row & 7);
+        int local = 0;
+        for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++local) {
+            int64_t m0, n0;
+            tile_coords(kMode, p, t, m0, n0);
+            const int64_t gm = m0 + row;
+            if (do_chain && n0 == 0) {
+                // One serial fp32 partial per ChunkPlan chunk (factored_norm.cpp:52-60);
+                // the finisher adds chunk partials in ascending order (:60), so K splits on
+                // chunk boundaries keep base_sq bitwise equal to the reference.  The loads of
+                // block i+1 are issued before the serial FADD chain of block i runs; stage i
+                // is released only after the chain consumed its registers (a release before
+                // the loads retire would let TMA overwrite the stage under them).
+                const int start = local * nkb;
+                int s = start % p.stages;
+                uint32_t ph = static_cast<uint32_t>((start / p.stages) & 1);
+                float partial = 0.0f;
+                int64_t kpos = int64_t(kb0) * kBK;
+                int64_t cur = kpos / p.chunk;
+                int64_t boundary = (cur + 1) * p.chunk;
+                uint4 nxt[8];
+                auto load = [&](uint4 (&dst)[8], int st, uint32_t sph) {
+                    mbar_wait(&full[st], sph);
+                    const uint8_t* rowp = smem + st * stage_bytes + row * 128;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((c ^ (row & 7)) << 4));
-                    float f[8];
-                    unpack_bf16x8(v, f);
+                    for (int c = 0; c < 8; ++c)
+                        dst[c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ swz) << 4));
+                };
+                load(nxt, s, ph);
+                for (int it = 0; it < nkb; ++it) {
+                    uint4 cv[8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) partial = __fadd_rn(partial, __fmul_rn(f[e], f[e]));
+                    for (int c = 0; c < 8; ++c) cv[c] = nxt[c];
+                    const int s_cur = s;
+                    if (++s == p.stages) { s = 0; ph ^= 1; }
+                    if (it + 1 < nkb) load(nxt, s, ph);
+                    if (kpos >= boundary) {
+                        if (gm < p.M) p.base_out[cur * p.M + gm] = partial;
+                        partial = 0.0f;
+                        ++cur;
+                        boundary += p.chunk;
+                    }
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        float f[8];
+                        unpack_bf16x8(cv[c], f);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            partial = __fadd_rn(partial, __fmul_rn(f[e], f[e]));
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[s_cur]);
+                    kpos += kBK;
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
+                if (gm < p.M) p.base_out[cur * p.M + gm] = partial;
             }
-            if (cur >= 0 && gm < p.M) p.base_out[cur * p.M + gm] = partial;
-        }
-        // wait for the accumulator
-        if (nkb > 0) {
-            mbar_wait(tmem_full, 0);
+            // ---- epilogue: TMEM accumulator -> rowdot / tile store
+            const int slot = local & 1;
+            mbar_wait(&tmem_full[slot], (local >> 1) & 1);
             tc_fence_after();
-        }
-        const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-        if (kMode == kTcRowdot) {
-            float acc = 0.0f;
-            for (int c0 = 0; c0 < p.bn; c0 += 32) {
-                uint32_t u[32];
-                tmem_ld_32x32b_x32(trow + c0, u);
-                tmem_ld_wait();
-                if (gm < p.M && nkb > 0) {
-                    const __nv_bfloat16* zr = p.Z + gm * p.ldz + n0 + c0;
+            const uint32_t trow = tmem_base + static_cast<uint32_t>(slot) * slot_cols +
+                                  (static_cast<uint32_t>(q * 32) << 16);
+            if (kMode == kTcRowdot) {
+                float acc = 0.0f;
+                for (int c0 = 0; c0 < p.bn; c0 += 32) {
+                    uint32_t u[32];
+                    tmem_ld_32x32b_x32(trow + c0, u);
+                    tmem_ld_wait();
+                    if (gm < p.M) {
+                        const __nv_bfloat16* zr = p.Z + gm * p.ldz + n0 + c0;
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        if (n0 + c0 + 8 * v < p.N) {
-                            float z[8];
-                            unpack_bf16x8(*reinterpret_cast<const uint4*>(zr + 8 * v), z);
+                        for (int v = 0; v < 4; ++v) {
+                            // columns past the tile (bn % 32 != 0) belong to the other slot
+                            if (c0 + 8 * v < p.bn && n0 + c0 + 8 * v < p.N) {
+                                float z[8];
+                                unpack_bf16x8(*reinterpret_cast<const uint4*>(zr + 8 * v), z);
 #pragma unroll
-                            for (int e = 0; e < 8; ++e)
-                                acc = fmaf(__uint_as_float(u[8 * v + e]), z[e], acc);
+                                for (int e = 0; e < 8; ++e)
+                                    acc = fmaf(__uint_as_float(u[8 * v + e]), z[e], acc);
+                            }
                         }
                     }
                 }
-            }
-            if (gm < p.M)
-                p.out[(int64_t(ks) * p.n_split + (n0 / p.bn)) * p.M + gm] = acc;
-        } else {
-            // gram tile store: out[(ks * tiles + tile) * 128*bn + row*bn + col]
-            float* dst = p.out + (int64_t(ks) * gridDim.x + blockIdx.x) * (int64_t(kBM) * p.bn) +
-                         int64_t(row) * p.bn;
-            for (int c0 = 0; c0 < p.bn; c0 += 32) {
-                uint32_t u[32];
-                tmem_ld_32x32b_x32(trow + c0, u);
-                tmem_ld_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tmem_empty[slot]);
+                if (gm < p.M) p.out[(int64_t(ks) * p.n_split + (n0 / p.bn)) * p.M + gm] = acc;
+            } else {
+                // gram tile store: out[(ks * tiles + t) * 128*bn + row*bn + col]
+                float* dst = p.out + (int64_t(ks) * p.tiles + t) * (int64_t(kBM) * p.bn) +
+                             int64_t(row) * p.bn;
+                for (int c0 = 0; c0 < p.bn; c0 += 32) {
+                    uint32_t u[32];
+                    tmem_ld_32x32b_x32(trow + c0, u);
+                    tmem_ld_wait();
 #pragma unroll
-                for (int e = 0; e < 32; e += 4) {
-                    float4 v = make_float4(__uint_as_float(u[e]), __uint_as_float(u[e + 1]),
-                                           __uint_as_float(u[e + 2]), __uint_as_float(u[e + 3]));
-                    if (nkb == 0) v = make_float4(0.f, 0.f, 0.f, 0.f);
-                    *reinterpret_cast<float4*>(dst + c0 + e) = v;
+                    for (int e = 0; e < 32; e += 4)
+                        *reinterpret_cast<float4*>(dst + c0 + e) =
+                            make_float4(__uint_as_float(u[e]), __uint_as_float(u[e + 1]),
+                                        __uint_as_float(u[e + 2]), __uint_as_float(u[e + 3]));
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tmem_empty[slot]);
             }
         }
     }
@@ -296,7 +357,7 @@ size_t smem_for(int bn, int stages) {
 }
 
 cudaError_t launch_tc(int mode, const CUtensorMap& tx, const CUtensorMap& ty, TcParams p,
-                      dim3 grid, cudaStream_t st) {
+                      dim3 grid, cudaStream_t st, const char* name) {
     static bool attr[2] = {false, false};
     const size_t smem = smem_for(p.bn, p.stages);
     cudaError_t e;
@@ -307,7 +368,9 @@ cudaError_t launch_tc(int mode, const CUtensorMap& tx, const CUtensorMap& ty, Tc
             if (e != cudaSuccess) return e;
             attr[0] = true;
         }
+        prof_begin(name, st);
         tc_rowdot<kTcRowdot><<<grid, kThreads, smem, st>>>(tx, ty, p);
+        prof_end(st);
     } else {
         if (!attr[1]) {
             e = cudaFuncSetAttribute(tc_rowdot<kTcStore>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -315,18 +378,20 @@ cudaError_t launch_tc(int mode, const CUtensorMap& tx, const CUtensorMap& ty, Tc
             if (e != cudaSuccess) return e;
             attr[1] = true;
         }
+        prof_begin(name, st);
         tc_rowdot<kTcStore><<<grid, kThreads, smem, st>>>(tx, ty, p);
+        prof_end(st);
     }
     return cudaGetLastError();
 }
 
-// (n_split, k_split) for a rowdot GEMM with m_tiles 128-row tiles: fill the 148 SMs in
-// as few waves as possible; BN <= 256.  Prefers N splits (keeps the base_sq chain of a
-// row in one CTA, bitwise) and uses K splits only when N splitting cannot fill.
+// (n_split, k_split) for a rowdot GEMM with m_tiles 128-row tiles on a budget of `ctas`
+// persistent CTAs: as few rounds as possible with balanced rounds; BN <= 256.  Prefers N
+// splits (a row's base_sq chain stays in one CTA) and K splits only when N splitting
+// cannot fill the budget.
 struct Split { int ns, ks, bn; };
 
-Split choose_split(int64_t m_tiles, int64_t r, int64_t kb_total, int max_ks) {
-    const int kSMs = 148;
+Split choose_split(int64_t m_tiles, int64_t r, int64_t kb_total, int max_ks, int ctas) {
     Split best{1, 1, 0};
     double best_score = -1.0;
     const int ns_min = static_cast<int>((r + 255) / 256);
@@ -336,9 +401,9 @@ Split choose_split(int64_t m_tiles, int64_t r, int64_t kb_total, int max_ks) {
         if (ns > ns_min && bn < 64) break;
         for (int ks = 1; ks <= max_ks && ks <= 8; ks *= 2) {
             if (ks > 1 && kb_total / ks < 4) break;
-            const int64_t ctas = m_tiles * ns * ks;
-            const int64_t waves = (ctas + kSMs - 1) / kSMs;
-            const double eff = double(ctas) / double(waves * kSMs);
+            const int64_t work = m_tiles * ns * ks;                 // tile-splits
+            const int64_t rounds = (work + ctas - 1) / ctas;
+            const double eff = double(work) / double(rounds * ctas);
             // penalise redundant operand traffic from splitting
             const double score = eff - 0.02 * (ns - ns_min) - 0.03 * (ks > 1 ? ks : 0);
             if (score > best_score + 1e-9) {
@@ -347,6 +412,7 @@ Split choose_split(int64_t m_tiles, int64_t r, int64_t kb_total, int max_ks) {
             }
         }
     }
+    if (best.bn == 0) best = {ns_min, 1, static_cast<int>(((r + ns_min - 1) / ns_min + 15) / 16 * 16)};
     return best;
 }
 
@@ -362,20 +428,79 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
     cudaError_t err = cudaSuccess;
     const int64_t r = a.r, d_out = a.d_out, d_in = a.d_in;
     const int64_t r_pad = (r + kBK - 1) / kBK * kBK;
-
-    // ---------------- G = A A^T (upper-triangle tiles, split-K) ----------------
-    const int nt = static_cast<int>((r + kBM - 1) / kBM);
-    const int tiles = nt * (nt + 1) / 2;
+    const int64_t m_tiles = (d_out + kBM - 1) / kBM;
     const int64_t kb_in = (d_in + kBK - 1) / kBK;
-    int g_ks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 / tiles, kb_in / 4)));
+
+    // SM budget: W A^T (the dominant GEMM, on the caller's stream) gets sms - kSide CTAs;
+    // the adapter-only chain Gram -> hi/lo -> B G runs concurrently on a side stream on
+    // the remaining kSide SMs (it does not depend on W), joined before the finisher.
+    const int sms = ws_sm_count(ws);
+    const int kMinSide = 8;
+
+    // ---------------- W A^T: cross partials + base_sq chain (main stream) --------------
+    // K splits only on ChunkPlan boundaries (each split = whole chunks)
+    const int64_t chunk_blocks = a.chunk_size / kBK;
+    const int64_t n_chunks = (d_in + a.chunk_size - 1) / a.chunk_size;
+    const Split su = choose_split(m_tiles, r, kb_in, static_cast<int>(std::min<int64_t>(n_chunks, 8)),
+                                  sms - kMinSide);
+    const int64_t u_work = m_tiles * su.ns;  // tiles per K split
+
+    const int64_t chunks_per_split = (n_chunks + su.ks - 1) / su.ks;
+    const int kbps = static_cast<int>(chunks_per_split * chunk_blocks);
+    const int ks = static_cast<int>((kb_in + kbps - 1) / kbps);
+    // the U GEMM takes one round of CTAs if it fits, the side chain the remaining SMs
+    const int main_ctas = static_cast<int>(std::min<int64_t>(u_work * ks, sms - kMinSide));
+    const int kSide = std::max(kMinSide, sms - main_ctas);
+    float* cross = static_cast<float*>(
+        ws_get(ws, kWsCross, size_t(ks) * su.ns * d_out * sizeof(float), &err));
+    if (err != cudaSuccess) return err;
+    float* base = static_cast<float*>(
+        ws_get(ws, kWsBase, size_t(n_chunks) * d_out * sizeof(float), &err));
+    if (err != cudaSuccess) return err;
+
+    // adapter-side buffers
+    const int nt = static_cast<int>((r + kBM - 1) / kBM);
+    const int gtiles = nt * (nt + 1) / 2;
+    int g_ks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kSide / gtiles, kb_in / 8)));
     const int g_kbps = static_cast<int>((kb_in + g_ks - 1) / g_ks);
     g_ks = static_cast<int>((kb_in + g_kbps - 1) / g_kbps);
     float* gpart = static_cast<float*>(
-        ws_get(ws, kWsGramPart, size_t(g_ks) * tiles * kBM * kBM * sizeof(float), &err));
+        ws_get(ws, kWsGramPart, size_t(g_ks) * gtiles * kBM * kBM * sizeof(float), &err));
     if (err != cudaSuccess) return err;
     __nv_bfloat16* g2 = static_cast<__nv_bfloat16*>(
         ws_get(ws, kWsGram2, size_t(r) * 2 * r_pad * sizeof(__nv_bfloat16), &err));
     if (err != cudaSuccess) return err;
+    const Split sb = choose_split(m_tiles, r, 2 * r_pad / kBK, 1, kSide);
+    float* ba = static_cast<float*>(ws_get(ws, kWsBa, size_t(sb.ns) * d_out * sizeof(float), &err));
+    if (err != cudaSuccess) return err;
+
+    cudaStream_t side = ws_side_stream(ws, &err);
+    if (err != cudaSuccess) return err;
+    cudaEvent_t ev_fork = ws_event(ws, 0, &err), ev_join = ws_event(ws, 1, &err);
+    if (err != cudaSuccess) return err;
+    if ((err = cudaEventRecord(ev_fork, st)) != cudaSuccess) return err;
+    if ((err = cudaStreamWaitEvent(side, ev_fork, 0)) != cudaSuccess) return err;
+
+    {
+        CUtensorMap tw, ta;
+        err = make_tmap_2d(&tw, kBF16, a.w, d_out, d_in, d_in * 2, kBK, kBM, true);
+        if (err != cudaSuccess) return err;
+        err = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, su.bn, true);
+        if (err != cudaSuccess) return err;
+        TcParams p{};
+        p.M = d_out; p.N = r; p.k_total = d_in; p.kb_per_split = kbps;
+        p.n_split = su.ns; p.bn = su.bn; p.stages = stages_for(su.bn);
+        p.x_kwrap = 0; p.chunk = a.chunk_size;
+        p.Z = static_cast<const __nv_bfloat16*>(a.b); p.ldz = r;
+        p.out = cross; p.base_out = base; p.do_chain = 1;
+        p.tiles = static_cast<int>(m_tiles * su.ns);
+        const int gx = std::min<int>(p.tiles, std::max(1, main_ctas / ks));
+        err = launch_tc(kTcRowdot, tw, ta, p, dim3(gx, ks), st, "u_rowdot_tc");
+        if (err != cudaSuccess) return err;
+        if (launches) ++*launches;
+    }
+
+    // ---------------- side stream: G = A A^T -> [G_hi | G_lo] -> ba_sq partials --------
     {
         CUtensorMap ta;
         err = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, kBM, true);
@@ -383,22 +508,19 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         TcParams p{};
         p.M = r; p.N = r; p.k_total = d_in; p.kb_per_split = g_kbps; p.n_split = 1;
         p.bn = kBM; p.stages = stages_for(kBM); p.chunk = a.chunk_size;
-        p.out = gpart; p.gram_nt = nt;
-        err = launch_tc(kTcStore, ta, ta, p, dim3(tiles, g_ks), st);
+        p.out = gpart; p.gram_nt = nt; p.tiles = gtiles;
+        const int gx = std::min(gtiles, std::max(1, kSide / g_ks));
+        err = launch_tc(kTcStore, ta, ta, p, dim3(gx, g_ks), side, "gram_tc");
         if (err != cudaSuccess) return err;
         const int64_t n = r * r_pad;
-        gram_reduce<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(gpart, g_ks, nt, r,
-                                                                             r_pad, g2);
+        prof_begin("gram_reduce", side);
+        gram_reduce<<<static_cast<unsigned>((n + 255) / 256), 256, 0, side>>>(gpart, g_ks, nt, r,
+                                                                               r_pad, g2);
+        prof_end(side);
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
         if (launches) *launches += 2;
     }
-
-    const int64_t m_tiles = (d_out + kBM - 1) / kBM;
-    // ---------------- ba_sq partials: rowdot(B [G_hi|G_lo], B) ----------------
-    const Split sb = choose_split(m_tiles, r, 2 * r_pad / kBK, 1);
-    float* ba = static_cast<float*>(ws_get(ws, kWsBa, size_t(sb.ns) * d_out * sizeof(float), &err));
-    if (err != cudaSuccess) return err;
     {
         CUtensorMap tb, tg;
         err = make_tmap_2d(&tb, kBF16, a.b, d_out, r, r * 2, kBK, kBM, true);
@@ -412,42 +534,14 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         p.x_kwrap = static_cast<int>(r_pad); p.chunk = a.chunk_size;
         p.Z = static_cast<const __nv_bfloat16*>(a.b); p.ldz = r;
         p.out = ba; p.do_chain = 0;
-        err = launch_tc(kTcRowdot, tb, tg, p, dim3(static_cast<unsigned>(m_tiles * sb.ns), 1), st);
+        p.tiles = static_cast<int>(m_tiles * sb.ns);
+        const int gx = std::min(p.tiles, kSide);
+        err = launch_tc(kTcRowdot, tb, tg, p, dim3(gx, 1), side, "ba_rowdot_tc");
         if (err != cudaSuccess) return err;
         if (launches) ++*launches;
     }
-
-    // ---------------- cross partials + base_sq chain: rowdot(W A^T, B) ----------------
-    // K splits only on ChunkPlan boundaries (each split = whole chunks)
-    const int64_t chunk_blocks = a.chunk_size / kBK;
-    const int64_t n_chunks = (d_in + a.chunk_size - 1) / a.chunk_size;
-    const Split su = choose_split(m_tiles, r, kb_in, static_cast<int>(std::min<int64_t>(n_chunks, 8)));
-    const int64_t chunks_per_split = (n_chunks + su.ks - 1) / su.ks;
-    const int kbps = static_cast<int>(chunks_per_split * chunk_blocks);
-    const int ks = static_cast<int>((kb_in + kbps - 1) / kbps);
-    float* cross = static_cast<float*>(
-        ws_get(ws, kWsCross, size_t(ks) * su.ns * d_out * sizeof(float), &err));
-    if (err != cudaSuccess) return err;
-    float* base = static_cast<float*>(
-        ws_get(ws, kWsBase, size_t(n_chunks) * d_out * sizeof(float), &err));
-    if (err != cudaSuccess) return err;
-    {
-        CUtensorMap tw, ta;
-        err = make_tmap_2d(&tw, kBF16, a.w, d_out, d_in, d_in * 2, kBK, kBM, true);
-        if (err != cudaSuccess) return err;
-        err = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, su.bn, true);
-        if (err != cudaSuccess) return err;
-        TcParams p{};
-        p.M = d_out; p.N = r; p.k_total = d_in; p.kb_per_split = kbps;
-        p.n_split = su.ns; p.bn = su.bn; p.stages = stages_for(su.bn);
-        p.x_kwrap = 0; p.chunk = a.chunk_size;
-        p.Z = static_cast<const __nv_bfloat16*>(a.b); p.ldz = r;
-        p.out = cross; p.base_out = base; p.do_chain = 1;
-        err = launch_tc(kTcRowdot, tw, ta, p,
-                        dim3(static_cast<unsigned>(m_tiles * su.ns), static_cast<unsigned>(ks)), st);
-        if (err != cudaSuccess) return err;
-        if (launches) ++*launches;
-    }
+    if ((err = cudaEventRecord(ev_join, side)) != cudaSuccess) return err;
+    if ((err = cudaStreamWaitEvent(st, ev_join, 0)) != cudaSuccess) return err;
 
     FinishArgs f{};
     f.base_part = base; f.base_parts = static_cast<int>(n_chunks);

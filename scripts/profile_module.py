@@ -1,0 +1,48 @@
+"""Runs a few DoRA module steps (row_norm + compose) eagerly for ncu captures.
+  python scripts/profile_module.py [--config c2] [--steps 3] [--bwd]"""
+import argparse
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--bwd", action="store_true")
+    a = ap.parse_args()
+    import torch
+    import paper_2603_22276_b200 as P
+    cfg = bench.CONFIGS[a.config]
+    d_out, d_in, r, rows = cfg["d_out"], cfg["d_in"], cfg["r"], cfg["tokens"]
+    s = 2.0 / math.sqrt(r)
+    dfx = P.Dfx(0)
+    cs, _ = P.plan_chunks(d_out, d_in)
+    bf = torch.bfloat16
+    W = torch.randn(d_out, d_in, device="cuda").to(bf)
+    A = torch.randn(r, d_in, device="cuda").to(bf)
+    B = torch.randn(d_out, r, device="cuda").to(bf)
+    base = torch.randn(rows, d_out, device="cuda").to(bf)
+    lora = torch.randn(rows, d_out, device="cuda").to(bf)
+    wn = torch.empty(d_out, device="cuda")
+    g = torch.empty(d_out, device="cuda")
+    m = torch.ones(d_out, device="cuda") * 90.0
+    delta, inner = torch.empty_like(base), torch.empty_like(base)
+    dl, db = torch.empty_like(base), torch.empty_like(base)
+    dm = torch.empty(d_out, device="cuda")
+    for _ in range(a.steps):
+        dfx.row_norm(W, A, B, s, cs, wn, m=m, g=g)
+        dfx.compose_fwd(base, lora, g, s, delta, inner if a.bwd else None)
+        if a.bwd:
+            dfx.compose_bwd(base, g, s, dl, db, inner=inner, w_norm=wn, d_mag=dm)
+    torch.cuda.synchronize()
+    print("ok", dfx.launches)
+
+
+if __name__ == "__main__":
+    main()

@@ -254,8 +254,11 @@ def run_gpu(args, rank, world, local_rank, dist):
     torch.cuda.synchronize()
 
     def step(b):
-        dfx.row_norm(b["W"], b["A"], b["B"], s, cs, b["wn"], m=b["m"], g=b["g"])
-        dfx.compose_fwd(b["base"], b["lora"], b["g"], s, b["delta"])
+        # --stage isolates one half of the module for analysis (the headline is "module")
+        if args.stage in ("module", "norm"):
+            dfx.row_norm(b["W"], b["A"], b["B"], s, cs, b["wn"], m=b["m"], g=b["g"])
+        if args.stage in ("module", "compose"):
+            dfx.compose_fwd(b["base"], b["lora"], b["g"], s, b["delta"])
 
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
@@ -478,6 +481,8 @@ def main():
     ap.add_argument("--prof-steps", type=int, default=40)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stage", default="module", choices=["module", "norm", "compose"],
+                    help="analysis only: time one half of the module")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

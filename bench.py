@@ -271,18 +271,46 @@ def run_gpu(args, rank, world, local_rank, dist):
     torch.cuda.synchronize()
     launches_per_step = dfx.launches - launches_before
 
-    # ---- capture one graph per buffer set
+    # ---- capture the module stream as CUDA graphs
+    # Modules are independent, so a graph holds npipe consecutive modules software-pipelined
+    # on two streams: module i's compose (HBM-bound, no shared memory) runs on stream B
+    # beside module i+1's row norm (tensor-bound) on stream A.  Explicit edges: compose i
+    # after norm i (it reads g_i); norm i+nbuf after compose i (it rewrites buffer set
+    # i % nbuf's g).  --no-pipeline captures one module per graph, strictly serial.
+    side = torch.cuda.Stream(device=dev)
+    npipe = args.pipeline if (args.pipeline > 1 and args.stage == "module"
+                          and args.steps % args.pipeline == 0) else 1
     graphs = []
-    for b in sets:
+    if npipe > 1:
+        sA, sB = stream.cuda_stream, side.cuda_stream
+        ev_norm = [torch.cuda.Event() for _ in range(npipe)]
+        ev_comp = [torch.cuda.Event() for _ in range(npipe)]
         gph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gph, stream=stream):
-            step(b)
+            for i in range(npipe):
+                b = sets[i % nbuf]
+                if i >= nbuf:
+                    stream.wait_event(ev_comp[i - nbuf])
+                dfx.row_norm(b["W"], b["A"], b["B"], s, cs, b["wn"], m=b["m"], g=b["g"], stream=sA)
+                ev_norm[i].record(stream)
+                side.wait_event(ev_norm[i])
+                dfx.compose_fwd(b["base"], b["lora"], b["g"], s, b["delta"], stream=sB)
+                ev_comp[i].record(side)
+            stream.wait_event(ev_comp[npipe - 1])
         graphs.append(gph)
+    else:
+        for b in sets:
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph, stream=stream):
+                step(b)
+            graphs.append(gph)
     torch.cuda.synchronize()
+    replays = args.steps // npipe
+    nrep = len(graphs)
 
     with torch.cuda.stream(stream):
-        for k in range(args.warmup):
-            graphs[k % nbuf].replay()
+        for k in range((args.warmup + npipe - 1) // npipe):
+            graphs[k % nrep].replay()
     torch.cuda.synchronize()
 
     # ---- timed region
@@ -293,8 +321,8 @@ def run_gpu(args, rank, world, local_rank, dist):
     with ClockSampler(local_rank) as clk:
         with torch.cuda.stream(stream):
             ev0.record(stream)
-            for k in range(args.steps):
-                graphs[k % nbuf].replay()
+            for k in range(replays):
+                graphs[k % nrep].replay()
             ev1.record(stream)
         torch.cuda.synchronize()
     if dist:
@@ -427,7 +455,10 @@ def run_gpu(args, rank, world, local_rank, dist):
                        "l2": f"inputs > L2 (W {d_out * d_in * 2 >> 20} MiB + base/lora "
                              f"{2 * rows * d_out * 2 >> 20} MiB per module), {nbuf} rotating "
                              f"module buffer sets",
-                       "timing": "CUDA graphs replayed on one stream, CUDA events, max over ranks"},
+                       "timing": "CUDA graphs replayed on one stream, CUDA events, max over ranks",
+                       "pipeline": (f"{npipe} modules per graph; module i's compose overlaps "
+                                    f"module i+1's norm on a second stream" if npipe > 1
+                                    else "serial")},
             "roofline": roofline, "roofline_norm_stage": norm_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
@@ -481,6 +512,8 @@ def main():
     ap.add_argument("--prof-steps", type=int, default=40)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pipeline", type=int, default=8,
+                    help="modules per graph, software-pipelined on two streams (1 = serial)")
     ap.add_argument("--stage", default="module", choices=["module", "norm", "compose"],
                     help="analysis only: time one half of the module")
     args = ap.parse_args()

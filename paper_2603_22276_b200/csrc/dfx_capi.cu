@@ -21,7 +21,6 @@
 #include "kernels/launch.h"
 
 namespace dfx {
-extern long long* dfx_exp_dbg_ptr;
 
 struct Workspace {
     int device = 0;
@@ -261,13 +260,6 @@ void dfx_ctx_destroy(dfx_ctx* ctx) {
 }
 
 int64_t dfx_ctx_launches(const dfx_ctx* ctx) { return ctx ? ctx->launches : 0; }
-
-// EXP: copy the MMA-thread timestamp buffer (development only)
-int dfx_exp_dbg(long long* host, int n) {
-    if (!dfx::dfx_exp_dbg_ptr) return -1;
-    cudaDeviceSynchronize();
-    return cudaMemcpy(host, dfx::dfx_exp_dbg_ptr, n * sizeof(long long), cudaMemcpyDeviceToHost);
-}
 
 int dfx_profile_enable(dfx_ctx* ctx, int on) {
     if (!ctx) return fail(DFX_EINVAL, "null context");

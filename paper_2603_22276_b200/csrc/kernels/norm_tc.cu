@@ -25,20 +25,18 @@
 #include "norm_common.cuh"
 
 namespace dfx {
-long long* dfx_exp_dbg_ptr = nullptr;  // EXP
 namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;                          // one 128-byte swizzle atom of bf16
 constexpr int kXStage = kBM * kBK * 2;           // 16 KiB
 constexpr int kThreads = 256;
-// Warp roles.  The SMSP arbiter issues highest-warp-id first, so the two single-thread
-// roles sit above the chain/epilogue warps that share their SMSP (wid % 4): otherwise
-// the chain's continuous FADD stream starves the MMA issuer and the TMA producer.
-// Chain/epilogue warps are 0..3 so that warp w owns TMEM lane quadrant w.
+// Warp roles (SMSP = wid % 4).  Epilogue warps are 0..3 so that warp w owns TMEM lane
+// quadrant w; the producer (4) and MMA issuer (5) share SMSPs 0 and 1 with epilogue warps
+// that are idle during the main loop, and the base_sq chain runs on warps 2 and 3, whose
+// SMSPs carry no pipeline role (see chain_units).
 constexpr int kWarpProducer = 4;
 constexpr int kWarpMma = 5;
-constexpr int kWarpAux = 6;      // 2-SM kernel: stage forwarder
 constexpr int kMaxSmem = 227 * 1024;
 
 enum TcMode { kTcRowdot = 0, kTcStore = 1 };
@@ -61,8 +59,6 @@ struct TcParams {
     int gram_nt;            // tiles per side
     int tiles;              // tiles per K split (the persistent loop's extent)
     int w_prefetch;         // K blocks of X (W) prefetched into L2 ahead of the loads
-    int exp_noload;         // EXP
-    long long* dbg;         // EXP: MMA-thread timestamps of CTA 0
 };
 
 __device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
@@ -74,12 +70,91 @@ __device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
     }
 }
 
-// The base_sq chain of a row tile is spread over the CTAs that share it (its N splits):
-// epilogue warp q chains its 32 rows in the tile whose N index is q * n_split / 4.
-__device__ __forceinline__ int chain_warps_of(int n_idx, int n_split) {
-    int c = 0;
-    for (int q = 0; q < 4; ++q) c += (q * n_split / 4) == n_idx;
-    return c;
+// The base_sq chain of a row tile (4 units of 32 rows) is spread over the CTAs that
+// share the tile (its N splits): unit u belongs to the CTA whose N index is u*n_split/4.
+// Inside a CTA only warps 2 and 3 chain (up to two units = two interleaved rows per
+// thread): they share SMSPs with no single-thread pipeline role, so the chain's
+// dependent FADD stream neither starves nor is starved by the producer / MMA issuer.
+struct ChainUnits {
+    int n;
+    int u[2];
+};
+
+__device__ __forceinline__ ChainUnits chain_units(int warp, int n_idx, int n_split) {
+    ChainUnits cu{0, {0, 0}};
+    if (warp != 2 && warp != 3) return cu;
+    int pos = 0;
+    for (int u = 0; u < 4; ++u) {
+        if ((u * n_split / 4) != n_idx) continue;
+        if ((pos & 1) == warp - 2 && cu.n < 2) cu.u[cu.n++] = u;
+        ++pos;
+    }
+    return cu;
+}
+
+__device__ __forceinline__ int chain_active_warps(int n_idx, int n_split) {
+    return (chain_units(2, n_idx, n_split).n > 0) + (chain_units(3, n_idx, n_split).n > 0);
+}
+
+// Serial fp32 sum of w*w for kRows rows of the tile (rows 32*u + lane), one partial per
+// ChainPlan chunk (factored_norm.cpp:52-60); partials go to base_out[chunk][row] and the
+// finisher adds them in ascending order (:60), so base_sq is bitwise the reference's.
+// The stage is released only after the chain consumed its registers.
+template <int kRows>
+__device__ __forceinline__ void chain_tile(const ChainUnits& cu, const uint8_t* smem,
+                                           int stage_bytes, uint64_t* ready, uint64_t* empty,
+                                           int stages, int start, int nkb, int kb0, int64_t chunk,
+                                           int64_t m0, int64_t M, float* base_out, int lane) {
+    int s = start % stages;
+    uint32_t ph = static_cast<uint32_t>((start / stages) & 1);
+    float part[kRows];
+    int row[kRows];
+#pragma unroll
+    for (int j = 0; j < kRows; ++j) {
+        part[j] = 0.0f;
+        row[j] = 32 * cu.u[j] + lane;
+    }
+    int64_t kpos = int64_t(kb0) * 64;
+    int64_t cur = kpos / chunk;
+    int64_t boundary = (cur + 1) * chunk;
+    for (int it = 0; it < nkb; ++it) {
+        mbar_wait(&ready[s], ph);
+        uint4 v[kRows][8];
+#pragma unroll
+        for (int j = 0; j < kRows; ++j) {
+            const uint8_t* rowp = smem + s * stage_bytes + row[j] * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                v[j][c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ (row[j] & 7)) << 4));
+        }
+        if (kpos >= boundary) {
+#pragma unroll
+            for (int j = 0; j < kRows; ++j) {
+                if (m0 + row[j] < M) base_out[cur * M + m0 + row[j]] = part[j];
+                part[j] = 0.0f;
+            }
+            ++cur;
+            boundary += chunk;
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            float f[kRows][8];
+#pragma unroll
+            for (int j = 0; j < kRows; ++j) unpack_bf16x8(v[j][c], f[j]);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+#pragma unroll
+                for (int j = 0; j < kRows; ++j)
+                    part[j] = __fadd_rn(part[j], __fmul_rn(f[j][e], f[j][e]));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        kpos += 64;
+        if (++s == stages) { s = 0; ph ^= 1; }
+    }
+#pragma unroll
+    for (int j = 0; j < kRows; ++j)
+        if (m0 + row[j] < M) base_out[cur * M + m0 + row[j]] = part[j];
 }
 
 // Tile t of split z (blockIdx.y): rowdot -> (m, n) = (t / n_split, t % n_split), adjacent
@@ -133,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmy);
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1 + (do_chain ? 4 : 0));
+            mbar_init(&empty[s], 1 + (do_chain ? 2 : 0));
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tmem_full[a], 1);
@@ -195,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++local) {
                 int64_t m0, n0;
                 tile_coords(kMode, p, t, m0, n0);
-                const int stand_in = do_chain ? 4 - chain_warps_of(t % p.n_split, p.n_split) : 0;
+                const int stand_in = do_chain ? 2 - chain_active_warps(t % p.n_split, p.n_split) : 0;
                 const int slot = local & 1;
                 const uint32_t tacc = tmem_base + static_cast<uint32_t>(slot) * slot_cols;
                 mbar_wait(&tmem_empty[slot], ((local >> 1) & 1) ^ 1);
@@ -223,61 +298,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ================= chain + epilogue (one row per thread) =================
         const int q = warp;               // TMEM lane quadrant
         const int row = q * 32 + lane;        // row inside the tile
-        const uint32_t swz = static_cast<uint32_t>(row & 7);
         int local = 0;
         for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++local) {
             int64_t m0, n0;
             tile_coords(kMode, p, t, m0, n0);
             const int64_t gm = m0 + row;
-            if (do_chain && (q * p.n_split / 4) == (t % p.n_split)) {
-                // One serial fp32 partial per ChunkPlan chunk (factored_norm.cpp:52-60);
-                // the finisher adds chunk partials in ascending order (:60), so K splits on
-                // chunk boundaries keep base_sq bitwise equal to the reference.  The loads of
-                // block i+1 are issued before the serial FADD chain of block i runs; stage i
-                // is released only after the chain consumed its registers (a release before
-                // the loads retire would let TMA overwrite the stage under them).
-                const int start = local * nkb;
-                int s = start % p.stages;
-                uint32_t ph = static_cast<uint32_t>((start / p.stages) & 1);
-                float partial = 0.0f;
-                int64_t kpos = int64_t(kb0) * kBK;
-                int64_t cur = kpos / p.chunk;
-                int64_t boundary = (cur + 1) * p.chunk;
-                uint4 nxt[8];
-                auto load = [&](uint4 (&dst)[8], int st, uint32_t sph) {
-                    mbar_wait(&full[st], sph);
-                    const uint8_t* rowp = smem + st * stage_bytes + row * 128;
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        dst[c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ swz) << 4));
-                };
-                load(nxt, s, ph);
-                for (int it = 0; it < nkb; ++it) {
-                    uint4 cv[8];
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) cv[c] = nxt[c];
-                    const int s_cur = s;
-                    if (++s == p.stages) { s = 0; ph ^= 1; }
-                    if (it + 1 < nkb) load(nxt, s, ph);
-                    if (kpos >= boundary) {
-                        if (gm < p.M) p.base_out[cur * p.M + gm] = partial;
-                        partial = 0.0f;
-                        ++cur;
-                        boundary += p.chunk;
-                    }
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        float f[8];
-                        unpack_bf16x8(cv[c], f);
-#pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            partial = __fadd_rn(partial, __fmul_rn(f[e], f[e]));
-                    }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[s_cur]);
-                    kpos += kBK;
-                }
-                if (gm < p.M) p.base_out[cur * p.M + gm] = partial;
+            if (do_chain) {
+                const ChainUnits cu = chain_units(warp, static_cast<int>(t % p.n_split), p.n_split);
+                if (cu.n == 2)
+                    chain_tile<2>(cu, smem, stage_bytes, full, empty, p.stages, local * nkb, nkb, kb0,
+                                  p.chunk, m0, p.M, p.base_out, lane);
+                else if (cu.n == 1)
+                    chain_tile<1>(cu, smem, stage_bytes, full, empty, p.stages, local * nkb, nkb, kb0,
+                                  p.chunk, m0, p.M, p.base_out, lane);
             }
             // ---- epilogue: TMEM accumulator -> rowdot / tile store
             const int slot = local & 1;
@@ -391,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&pfull[s], 1);
-            mbar_init(&empty[s], 1 + (do_chain ? 4 : 0));
+            mbar_init(&empty[s], 1 + (do_chain ? 2 : 0));
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tmem_full[a], 1);
@@ -432,11 +465,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (it + pf < nkb)
                         tma_prefetch_2d(&tmx, (kb0 + it + pf) * kBK, static_cast<int32_t>(m0));
                     mbar_wait(&empty[s], ph ^ 1);
-                    if (p.exp_noload && it >= p.stages) {  // EXP: no new data after one ring
-                        if (leader) mbar_arrive(&full[s]);
-                        if (++s == p.stages) { s = 0; ph ^= 1; }
-                        continue;
-                    }
                     if (leader) mbar_arrive_expect_tx(&full[s], 2 * stage_bytes);
                     const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
                     uint8_t* sx = smem + s * stage_bytes;
@@ -461,9 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&tmem_empty[slot], ((local >> 1) & 1) ^ 1);
                 tc_fence_after();
                 for (int it = 0; it < nkb; ++it) {
-                    if (p.dbg && blockIdx.x == 0 && local == 0) p.dbg[2 * it] = clock64();
                     mbar_wait(&full[s], ph);
-                    if (p.dbg && blockIdx.x == 0 && local == 0) p.dbg[2 * it + 1] = clock64();
                     tc_fence_after();
                     const uint32_t sx = smem_u32(smem + s * stage_bytes);
                     const uint32_t sy = sx + kXStage;
@@ -479,81 +505,45 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma_commit_pair_mc(&tmem_full[slot], 0x3);
             }
         }
-    } else if (nkb > 0 && warp == kWarpAux) {
-        // ================= stage forwarder (leader CTA) =================
-        // Off the MMA issue path: tell the peer's chain warps that a stage landed (its
-        // TMA completes on the leader's barrier), and on tiles without a chain stand in
-        // for both CTAs' chain-warp arrivals on the empty barriers.
-        if (leader && lane == 0) {
-            int s = 0;
-            uint32_t ph = 0;
-            for (int t = pair; t < p.tiles; t += npairs) {
-                const int stand_in = do_chain ? 4 - chain_warps_of(t % p.n_split, p.n_split) : 0;
-                for (int it = 0; it < nkb; ++it) {
-                    mbar_wait(&full[s], ph);
-                    mbar_arrive_remote(mapa_shared(smem_u32(&pfull[s]), 1), 1);
-                    if (stand_in) {
-                        mbar_arrive_cnt(&empty[s], stand_in);
-                        mbar_arrive_remote(mapa_shared(smem_u32(&empty[s]), 1), stand_in);
-                    }
-                    if (++s == p.stages) { s = 0; ph ^= 1; }
-                }
-            }
-        }
     } else if (nkb > 0 && warp < 4) {
-        // ================= chain + epilogue (own 128 rows, one row per thread) =============
+        // ================= forwarder + chain + epilogue (own 128 rows) =================
         const int q = warp;
         const int row = q * 32 + lane;
-        const uint32_t swz = static_cast<uint32_t>(row & 7);
         uint64_t* ready = leader ? full : pfull;   // "stage s landed" as seen by this CTA
+        // Leader warp 0 (idle until the epilogue) forwards "stage landed" to the peer's
+        // chain warps (the peer's TMA completes on the leader's barrier) and stands in for
+        // the chain warps that do not chain this tile, in both CTAs.
+        int fs = 0;
+        uint32_t fph = 0;
+        auto forward_tile = [&](int t) {
+            if (lane == 0) {
+                const int stand_in = do_chain ? 2 - chain_active_warps(t % p.n_split, p.n_split) : 0;
+                for (int it = 0; it < nkb; ++it) {
+                    mbar_wait(&full[fs], fph);
+                    mbar_arrive_remote(mapa_shared(smem_u32(&pfull[fs]), 1), 1);
+                    if (stand_in) {
+                        mbar_arrive_cnt(&empty[fs], stand_in);
+                        mbar_arrive_remote(mapa_shared(smem_u32(&empty[fs]), 1), stand_in);
+                    }
+                    if (++fs == p.stages) { fs = 0; fph ^= 1; }
+                }
+            }
+            __syncwarp();
+        };
         int local = 0;
         for (int t = pair; t < p.tiles; t += npairs, ++local) {
             const int64_t m0 = int64_t(t / p.n_split) * (2 * kBM) + int64_t(rank) * kBM;
             const int64_t n0 = int64_t(t % p.n_split) * p.bn;
             const int64_t gm = m0 + row;
-            if (do_chain && (q * p.n_split / 4) == (t % p.n_split)) {
-                const int start = local * nkb;
-                int s = start % p.stages;
-                uint32_t ph = static_cast<uint32_t>((start / p.stages) & 1);
-                float partial = 0.0f;
-                int64_t kpos = int64_t(kb0) * kBK;
-                int64_t cur = kpos / p.chunk;
-                int64_t boundary = (cur + 1) * p.chunk;
-                uint4 nxt[8];
-                auto load = [&](uint4 (&dst)[8], int st, uint32_t sph) {
-                    mbar_wait_cluster(&ready[st], sph);
-                    const uint8_t* rowp = smem + st * stage_bytes + row * 128;
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        dst[c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ swz) << 4));
-                };
-                load(nxt, s, ph);
-                for (int it = 0; it < nkb; ++it) {
-                    uint4 cv[8];
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) cv[c] = nxt[c];
-                    const int s_cur = s;
-                    if (++s == p.stages) { s = 0; ph ^= 1; }
-                    if (it + 1 < nkb) load(nxt, s, ph);
-                    if (kpos >= boundary) {
-                        if (gm < p.M) p.base_out[cur * p.M + gm] = partial;
-                        partial = 0.0f;
-                        ++cur;
-                        boundary += p.chunk;
-                    }
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        float f[8];
-                        unpack_bf16x8(cv[c], f);
-#pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            partial = __fadd_rn(partial, __fmul_rn(f[e], f[e]));
-                    }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[s_cur]);
-                    kpos += kBK;
-                }
-                if (gm < p.M) p.base_out[cur * p.M + gm] = partial;
+            if (leader && warp == 0) forward_tile(t);
+            if (do_chain) {
+                const ChainUnits cu = chain_units(warp, static_cast<int>(t % p.n_split), p.n_split);
+                if (cu.n == 2)
+                    chain_tile<2>(cu, smem, stage_bytes, ready, empty, p.stages, local * nkb, nkb, kb0,
+                                  p.chunk, m0, p.M, p.base_out, lane);
+                else if (cu.n == 1)
+                    chain_tile<1>(cu, smem, stage_bytes, ready, empty, p.stages, local * nkb, nkb, kb0,
+                                  p.chunk, m0, p.M, p.base_out, lane);
             }
             const int slot = local & 1;
             mbar_wait(&tmem_full[slot], (local >> 1) & 1);
@@ -748,21 +738,8 @@ Split choose_split(int64_t m_tiles, int64_t r, int64_t kb_total, int max_ks, int
 
 }  // namespace
 
-// EXP: development knobs for the W.A^T GEMM (removed once tuned)
-void exp_knobs(TcParams& p) {
-    if (std::getenv("DFX_EXP_NOCHAIN")) p.do_chain = 0;
-    if (const char* e = std::getenv("DFX_EXP_PF")) p.w_prefetch = std::atoi(e);
-    if (const char* e = std::getenv("DFX_EXP_STAGES")) p.stages = std::atoi(e);
-    p.exp_noload = std::getenv("DFX_EXP_NOLOAD") ? 1 : 0;
-    static long long* dbg = nullptr;
-    if (std::getenv("DFX_EXP_DBG")) {
-        if (!dbg) cudaMalloc(&dbg, 4096 * sizeof(long long));
-        p.dbg = dbg;
-        dfx_exp_dbg_ptr = dbg;
-    }
-}
-
-// DFX_NORM_PAIR=0 selects the 1-SM kernel for the W.A^T GEMM (A/B measurements).
+// DFX_NORM_PAIR=0 selects the 1-SM kernel for the W.A^T GEMM (A/B measurements; the
+// two are within ~1% at module level on C2, the 2-SM one is the faster GEMM).
 bool pair_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("DFX_NORM_PAIR");
@@ -857,12 +834,10 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
             err = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, su.bn / 2, true);
             if (err != cudaSuccess) return err;
             p.stages = stages_for_pair(su.bn);
-            exp_knobs(p);                                                                // EXP
             p.tiles = static_cast<int>(pm_tiles * su.ns);
             const int pairs = std::min<int>(p.tiles, std::max(1, main_ctas / (2 * ks)));
             err = launch_tc_pair(tw, ta, p, pairs, ks, st, "u_rowdot_tc");
         } else {
-            exp_knobs(p);                                                                // EXP
             p.tiles = static_cast<int>(m_tiles * su.ns);
             const int gx = std::min<int>(p.tiles, std::max(1, main_ctas / ks));
             err = launch_tc(kTcRowdot, tw, ta, p, dim3(gx, ks), st, "u_rowdot_tc");

@@ -79,6 +79,13 @@ void* ws_get(Workspace* ws, int slot, size_t bytes, cudaError_t* err) {
     return ws->ptr[slot];
 }
 
+void* ws_get_zeroed(Workspace* ws, int slot, size_t bytes, cudaError_t* err) {
+    const bool fresh = ws->cap[slot] < (bytes ? bytes : 16);
+    void* p = ws_get(ws, slot, bytes, err);
+    if (*err == cudaSuccess && fresh) *err = cudaMemset(p, 0, ws->cap[slot]);
+    return p;
+}
+
 namespace {
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,

@@ -56,6 +56,8 @@ void prof_end(cudaStream_t st);
 
 struct Workspace;  // owned by the context (dfx_capi.cu)
 void* ws_get(Workspace* ws, int slot, size_t bytes, cudaError_t* err);
+// Same, zero-filled when (re)allocated (kernels keep it zero between calls).
+void* ws_get_zeroed(Workspace* ws, int slot, size_t bytes, cudaError_t* err);
 // Context-owned side stream (non-blocking) and fork/join events for intra-call concurrency.
 cudaStream_t ws_side_stream(Workspace* ws, cudaError_t* err);
 cudaEvent_t ws_event(Workspace* ws, int idx, cudaError_t* err);

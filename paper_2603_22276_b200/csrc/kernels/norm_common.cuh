@@ -18,6 +18,7 @@ enum WsSlot : int {
     kWsBase = 4,       // base_sq partials     [k_split][d_out] fp32
     kWsGram = 5,       // G fp32               [r][r]          (SIMT path)
     kWsTerms = 6,      // base_sq/cross/ba_sq  [3][d_out]      (when caller wants none)
+    kWsGramCount = 7,  // per-tile split counters for the fused Gram reduction (zeroed)
     kWsCount = 8
 };
 

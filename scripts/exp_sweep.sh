@@ -1,3 +1,2 @@
-for cfg in "DFX_NORM_PAIR=1" "DFX_NORM_PAIR=0" "DFX_NORM_PAIR=1" "DFX_NORM_PAIR=0"; do
-  echo "== $cfg"; env $cfg timeout 120 python bench.py --steps 4000 --e2e-steps 0 --no-cpu-baseline --prof-steps 2 2>&1 | grep -o 'timed.*'; done
-timeout 300 python bench.py > gpurun_out/bench6.json 2> gpurun_out/bench6.err; echo rc=$?; tail -3 gpurun_out/bench6.err | cut -c1-300
+for cfg in "" "DFX_NORM_BA=after"; do
+  for st in norm module; do echo "== $cfg $st"; env $cfg timeout 120 python bench.py --steps 2000 --e2e-steps 0 --no-cpu-baseline --prof-steps 2 --stage $st 2>&1 | grep -o 'timed.*'; done; done

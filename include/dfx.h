@@ -104,6 +104,24 @@ int dfx_row_norm(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A, co
                  const float* m, dfx_dtype mag_dtype, float* w_norm, float* g, float* terms,
                  dfx_stream_t stream);
 
+/* d_in-split (FSDP2-style) factored norm — the exchange the paper leaves open
+ * (PAPER.md:1073-1078).  Step 1 on every rank: the terms of this rank's K slice,
+ * W_k [d_out x d_in_k], A_k [r x d_in_k], full B [d_out x r]:
+ *   gram [r x r] = A_k A_k^T, base_sq [d_out] = serial chain over the slice (chunked by
+ *   chunk_size), cross [d_out] = rowdot(W_k A_k^T, B)   (all fp32)
+ * The caller sums {gram, base_sq, cross} over ranks (one all-reduce of r*r + 2*d_out
+ * floats) and then calls dfx_norm_finish, which needs no W. */
+int dfx_norm_partial(dfx_ctx* ctx, dfx_dtype dtype, const void* W_k, const void* A_k,
+                     const void* B, int64_t d_out, int64_t d_in_k, int64_t r, int64_t chunk_size,
+                     float* gram, float* base_sq, float* cross, dfx_stream_t stream);
+
+/* Step 2: ba_sq = rowquad(B, G) from the reduced Gram, assemble_norm, round to `dtype`,
+ * magnitude (when m != NULL).  terms (3 x d_out) optional, like dfx_row_norm. */
+int dfx_norm_finish(dfx_ctx* ctx, dfx_dtype dtype, const void* B, const float* gram,
+                    const float* base_sq, const float* cross, int64_t d_out, int64_t r, double s,
+                    const float* m, dfx_dtype mag_dtype, float* w_norm, float* g, float* terms,
+                    dfx_stream_t stream);
+
 /* stable_compose / fused_compose / dual_output_compose (compose.hpp:43,53-57,62-68):
  * delta = (g-1)*base + g*(s*lora) in the canonical rounding order, bitwise equal to
  * the reference; inner = s*lora + base when inner != NULL (dual output). */

@@ -67,6 +67,10 @@ SIGNATURES = {
     "dfx_magnitude_scale": (_int, [_vp, _int, _vp, _vp, _i64, _vp, _vp]),
     "dfx_row_norm": (_int, [_vp, _int, _vp, _vp, _vp, _i64, _i64, _i64, _f64, _i64, _vp, _int,
                             _vp, _vp, _vp, _vp]),
+    "dfx_norm_partial": (_int, [_vp, _int, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
+                                _vp]),
+    "dfx_norm_finish": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _i64, _i64, _f64, _vp, _int, _vp, _vp,
+                               _vp, _vp]),
     "dfx_compose_fwd": (_int, [_vp, _int, _vp, _vp, _vp, _f64, _i64, _i64, _vp, _vp, _vp]),
     "dfx_compose_bwd": (_int, [_vp, _int, _vp, _vp, _f64, _vp, _vp, _i64, _i64, _vp, _vp, _vp,
                                _vp]),
@@ -165,6 +169,25 @@ class Dfx:
                                           float(s), int(chunk_size), _ptr(m),
                                           dt if mag_dtype is None else mag_dtype, _ptr(w_norm),
                                           _ptr(g), _ptr(terms), _stream(stream)))
+
+    def norm_partial(self, W_k, A_k, B, chunk_size, gram, base_sq, cross, stream=None):
+        """d_in-split step 1: this rank's K-slice terms (sum them over ranks)."""
+        d_out, d_in_k = W_k.shape
+        r = A_k.shape[0]
+        self._check(self.lib.dfx_norm_partial(self.ctx, _dtype_code(W_k), _ptr(W_k), _ptr(A_k),
+                                              _ptr(B), d_out, d_in_k, r, int(chunk_size),
+                                              _ptr(gram), _ptr(base_sq), _ptr(cross),
+                                              _stream(stream)))
+
+    def norm_finish(self, B, gram, base_sq, cross, s, w_norm, m=None, g=None, terms=None,
+                    mag_dtype=None, stream=None):
+        """d_in-split step 2 from the reduced {gram, base_sq, cross}."""
+        d_out, r = B.shape
+        dt = _dtype_code(B)
+        self._check(self.lib.dfx_norm_finish(self.ctx, dt, _ptr(B), _ptr(gram), _ptr(base_sq),
+                                             _ptr(cross), d_out, r, float(s), _ptr(m),
+                                             dt if mag_dtype is None else mag_dtype, _ptr(w_norm),
+                                             _ptr(g), _ptr(terms), _stream(stream)))
 
     def assemble(self, base_sq, cross, ba_sq, two_s, s2, out, round_to=F32, n=None,
                  stream=None):

@@ -405,6 +405,52 @@ int dfx_row_norm(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A, co
                     w_norm, g, dtype, stream, "dfx_row_norm");
 }
 
+int dfx_norm_partial(dfx_ctx* ctx, dfx_dtype dtype, const void* W_k, const void* A_k,
+                     const void* B, int64_t d_out, int64_t d_in_k, int64_t r, int64_t chunk_size,
+                     float* gram, float* base_sq, float* cross, dfx_stream_t stream) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    rc = check_norm_args(dtype, W_k, A_k, B, d_out, d_in_k, r, chunk_size);
+    if (rc) return rc;
+    if (!gram || (d_out > 0 && (!base_sq || !cross)))
+        return fail(DFX_EINVAL, "dfx_norm_partial: null output");
+    dfx::NormArgs a{};
+    a.dt = dtype; a.w = W_k; a.a = A_k; a.b = B;
+    a.d_out = d_out; a.d_in = d_in_k; a.r = r; a.s = 1.0; a.chunk_size = chunk_size;
+    a.base_sq = base_sq; a.cross = cross;
+    a.round_dt = dtype; a.mag_dt = dtype;
+    a.mode = dfx::kNormPartial; a.gram_out = gram;
+    int launches = 0;
+    const cudaError_t e = dfx::launch_norm(a, &ctx->ws, stream, &launches);
+    ctx->launches += launches;
+    return finish_call(e, "dfx_norm_partial");
+}
+
+int dfx_norm_finish(dfx_ctx* ctx, dfx_dtype dtype, const void* B, const float* gram,
+                    const float* base_sq, const float* cross, int64_t d_out, int64_t r, double s,
+                    const float* m, dfx_dtype mag_dtype, float* w_norm, float* g, float* terms,
+                    dfx_stream_t stream) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (!valid_dtype(dtype)) return fail(DFX_EINVAL, "dfx_norm_finish: dtype");
+    if (d_out < 0 || r < 1) return fail(DFX_EINVAL, "factored_norm: rank must be >= 1");
+    if (d_out > 0 && (!B || !gram || !base_sq || !cross))
+        return fail(DFX_EINVAL, "dfx_norm_finish: null operand");
+    if (m && (!g || !valid_dtype(mag_dtype))) return fail(DFX_EINVAL, "dfx_norm_finish: m without g");
+    dfx::NormArgs a{};
+    a.dt = dtype; a.b = B; a.d_out = d_out; a.d_in = 0; a.r = r; a.s = s; a.chunk_size = 64;
+    a.base_sq = terms ? terms : nullptr;
+    a.cross = terms ? terms + d_out : nullptr;
+    a.ba_sq = terms ? terms + 2 * d_out : nullptr;
+    a.m = m; a.w_norm = w_norm; a.g = g;
+    a.round_dt = dtype; a.mag_dt = mag_dtype;
+    a.mode = dfx::kNormFinish; a.gram_in = gram; a.base_in = base_sq; a.cross_in = cross;
+    int launches = 0;
+    const cudaError_t e = dfx::launch_norm(a, &ctx->ws, stream, &launches);
+    ctx->launches += launches;
+    return finish_call(e, "dfx_norm_finish");
+}
+
 int dfx_assemble_norm(dfx_ctx* ctx, const float* base_sq, const float* cross,
                       const float* ba_sq, double two_s, double s2, int64_t n,
                       dfx_dtype round_to, float* w_norm, dfx_stream_t stream) {

@@ -46,7 +46,16 @@ struct NormArgs {
     float* g;         // dtype-rounded scale (fp32 storage)
     int round_dt;     // dtype the norm is rounded to (kF32 => plain fp32 assemble)
     int mag_dt;       // working dtype of the magnitude division
+    // d_in split (FSDP2-style): kNormPartial computes this rank's K-slice terms
+    // (gram_out, base_sq, cross); kNormFinish completes from reduced inputs.
+    int mode;
+    float* gram_out;        // partial: fp32 [r x r]
+    const float* gram_in;   // finish: reduced fp32 Gram [r x r]
+    const float* base_in;   // finish: reduced base_sq [d_out]
+    const float* cross_in;  // finish: reduced cross [d_out]
 };
+
+enum NormMode : int { kNormFull = 0, kNormPartial = 1, kNormFinish = 2 };
 
 // Per-launch device timing (dfx_profile_enable): launch sites bracket each kernel
 // with these; they are no-ops unless the calling thread is inside a call on a

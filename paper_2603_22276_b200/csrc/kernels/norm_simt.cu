@@ -217,18 +217,42 @@ cudaError_t norm_simt_impl(const NormArgs& a, Workspace* ws, cudaStream_t st, in
     f.round_dt = a.round_dt; f.w_norm = a.w_norm;
     f.m = a.m; f.mag_dt = a.mag_dt; f.g = a.m ? a.g : nullptr;
 
+    if (a.mode == kNormFinish) {
+        // d_in split, step 2: ba_sq from the reduced Gram, then assemble / round / g
+        f.base_part = a.base_in; f.base_parts = 1;
+        if (a.s != 0.0) {  // s == 0: the reference skips cross / ba_sq (factored_norm.cpp:37)
+            const int64_t nt = (a.r + kBN - 1) / kBN;
+            float* ba = static_cast<float*>(ws_get(ws, kWsBa, nt * a.d_out * sizeof(float), &err));
+            if (err != cudaSuccess) return err;
+            prof_begin("simt_ba_rowdot", st);
+            simt_gemm<T, float, kRowdot, false>
+                <<<dim3(blocks_for(a.d_out, kBM), static_cast<unsigned>(nt)), 256, 0, st>>>(
+                    B, a.r, a.gram_in, a.r, B, a.r, a.d_out, a.r, a.r, a.chunk_size, ba, nullptr);
+            prof_end(st);
+            if (launches) ++*launches;
+            f.cross_part = a.cross_in; f.cross_parts = 1;
+            f.ba_part = ba; f.ba_parts = static_cast<int>(nt);
+        }
+        err = cudaGetLastError();
+        if (err != cudaSuccess) return err;
+        if (launches) ++*launches;
+        return launch_finish(f, st);
+    }
+
     float* base = static_cast<float*>(ws_get(ws, kWsBase, a.d_out * sizeof(float), &err));
     if (err != cudaSuccess) return err;
     f.base_part = base; f.base_parts = 1;
 
-    if (a.s == 0.0) {
+    if (a.s == 0.0 && a.mode == kNormFull) {
         prof_begin("base_chain", st);
         base_chain<T><<<blocks_for(a.d_out, 32), 256, 0, st>>>(W, a.d_out, a.d_in, a.chunk_size, base);
         prof_end(st);
         if (launches) ++*launches;
     } else {
         const int64_t nt = (a.r + kBN - 1) / kBN;
-        float* G = static_cast<float*>(ws_get(ws, kWsGram, a.r * a.r * sizeof(float), &err));
+        float* G = a.mode == kNormPartial
+                       ? a.gram_out
+                       : static_cast<float*>(ws_get(ws, kWsGram, a.r * a.r * sizeof(float), &err));
         if (err != cudaSuccess) return err;
         float* cross = static_cast<float*>(ws_get(ws, kWsCross, nt * a.d_out * sizeof(float), &err));
         if (err != cudaSuccess) return err;
@@ -242,11 +266,13 @@ cudaError_t norm_simt_impl(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         prof_end(st);
         // ba_sq partials: rowdot(B G, B); G is exactly symmetric (p,q and q,p use the
         // same products in the same order), so Y = G serves as (G^T)
-        prof_begin("simt_ba_rowdot", st);
-        simt_gemm<T, float, kRowdot, false>
-            <<<dim3(blocks_for(a.d_out, kBM), static_cast<unsigned>(nt)), 256, 0, st>>>(
-                B, a.r, G, a.r, B, a.r, a.d_out, a.r, a.r, a.chunk_size, ba, nullptr);
-        prof_end(st);
+        if (a.mode == kNormFull) {
+            prof_begin("simt_ba_rowdot", st);
+            simt_gemm<T, float, kRowdot, false>
+                <<<dim3(blocks_for(a.d_out, kBM), static_cast<unsigned>(nt)), 256, 0, st>>>(
+                    B, a.r, G, a.r, B, a.r, a.d_out, a.r, a.r, a.chunk_size, ba, nullptr);
+            prof_end(st);
+        }
         // cross partials + base_sq chain: rowdot(W A^T, B)
         prof_begin("simt_u_rowdot", st);
         simt_gemm<T, T, kRowdot, true>
@@ -255,8 +281,9 @@ cudaError_t norm_simt_impl(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         prof_end(st);
         if (launches) *launches += 3;
         f.cross_part = cross; f.cross_parts = static_cast<int>(nt);
-        f.ba_part = ba; f.ba_parts = static_cast<int>(nt);
+        if (a.mode == kNormFull) { f.ba_part = ba; f.ba_parts = static_cast<int>(nt); }
     }
+    if (a.mode == kNormPartial) { f.w_norm = nullptr; f.g = nullptr; f.ba_sq = nullptr; }
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     if (launches) ++*launches;
@@ -303,7 +330,9 @@ int norm_uses_tensor_cores(int dt, int64_t d_out, int64_t d_in, int64_t r) {
 cudaError_t launch_norm(const NormArgs& a, Workspace* ws, cudaStream_t st, int* launches) {
     if (a.d_out == 0) return cudaSuccess;
     // the tensor-core chain walks 64-wide K blocks: chunk boundaries must align to them
-    if (a.s != 0.0 && a.chunk_size % 64 == 0 && norm_tc_supported(a.dt, a.d_out, a.d_in, a.r))
+    const int64_t tc_din = a.mode == kNormFinish ? 64 : a.d_in;  // finish reads no W
+    if ((a.s != 0.0 || a.mode == kNormPartial) && a.chunk_size % 64 == 0 &&
+        norm_tc_supported(a.dt, a.d_out, tc_din, a.r))
         return launch_norm_tc(a, ws, st, launches);
     switch (a.dt) {
         case kF32: return norm_simt_impl<float>(a, ws, st, launches);

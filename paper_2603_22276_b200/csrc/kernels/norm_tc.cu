@@ -597,7 +597,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // G mirrored from the upper triangle, so the hi/lo operand is exactly symmetric.
 __global__ void __launch_bounds__(256) gram_reduce(const float* __restrict__ part, int k_split,
                                                    int nt, int64_t r, int64_t r_pad,
-                                                   __nv_bfloat16* __restrict__ g2) {
+                                                   __nv_bfloat16* __restrict__ g2,
+                                                   float* __restrict__ gout) {
     const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= r * r_pad) return;
     const int64_t i = idx / r_pad, j = idx % r_pad;
@@ -613,10 +614,24 @@ __global__ void __launch_bounds__(256) gram_reduce(const float* __restrict__ par
         for (int s = 1; s < k_split; ++s)
             gsum = __fadd_rn(gsum, part[(int64_t(s) * tiles + tile) * kBM * kBM + off]);
     }
+    if (gout && j < r) gout[i * r + j] = gsum;       // d_in-split partial: fp32 Gram out
+    if (!g2) return;
     const __nv_bfloat16 hi = __float2bfloat16_rn(gsum);
     const __nv_bfloat16 lo = __float2bfloat16_rn(__fsub_rn(gsum, __bfloat162float(hi)));
     g2[i * 2 * r_pad + j] = hi;
     g2[i * 2 * r_pad + r_pad + j] = lo;
+}
+
+// d_in-split finish: the all-reduced fp32 Gram -> [G_hi | G_lo] (bf16, K padded with 0).
+__global__ void __launch_bounds__(256) gram_split(const float* __restrict__ g, int64_t r,
+                                                  int64_t r_pad, __nv_bfloat16* __restrict__ g2) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= r * r_pad) return;
+    const int64_t i = idx / r_pad, j = idx % r_pad;
+    const float v = j < r ? g[i * r + j] : 0.0f;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    g2[i * 2 * r_pad + j] = hi;
+    g2[i * 2 * r_pad + r_pad + j] = __float2bfloat16_rn(__fsub_rn(v, __bfloat162float(hi)));
 }
 
 int stages_for(int bn) {
@@ -753,9 +768,14 @@ bool norm_tc_supported(int dt, int64_t d_out, int64_t d_in, int64_t r) {
            d_out >= 1 && d_in < (int64_t(1) << 31) && d_out < (int64_t(1) << 31);
 }
 
+cudaError_t launch_norm_finish_tc(const NormArgs& a, Workspace* ws, cudaStream_t st,
+                                  int* launches);
+
 cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, int* launches) {
+    if (a.mode == kNormFinish) return launch_norm_finish_tc(a, ws, st, launches);
     if (!norm_tc_supported(a.dt, a.d_out, a.d_in, a.r)) return cudaErrorNotSupported;
     cudaError_t err = cudaSuccess;
+    const bool partial = a.mode == kNormPartial;
     const int64_t r = a.r, d_out = a.d_out, d_in = a.d_in;
     const int64_t r_pad = (r + kBK - 1) / kBK * kBK;
     const int64_t m_tiles = (d_out + kBM - 1) / kBM;
@@ -860,14 +880,14 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         if (err != cudaSuccess) return err;
         const int64_t n = r * r_pad;
         prof_begin("gram_reduce", side);
-        gram_reduce<<<static_cast<unsigned>((n + 255) / 256), 256, 0, side>>>(gpart, g_ks, nt, r,
-                                                                               r_pad, g2);
+        gram_reduce<<<static_cast<unsigned>((n + 255) / 256), 256, 0, side>>>(
+            gpart, g_ks, nt, r, r_pad, partial ? nullptr : g2, partial ? a.gram_out : nullptr);
         prof_end(side);
         err = cudaGetLastError();
         if (err != cudaSuccess) return err;
         if (launches) *launches += 2;
     }
-    {
+    if (!partial) {
         CUtensorMap tb, tg;
         err = make_tmap_2d(&tb, kBF16, a.b, d_out, r, r * 2, kBK, kBM, true);
         if (err != cudaSuccess) return err;
@@ -892,11 +912,62 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
     FinishArgs f{};
     f.base_part = base; f.base_parts = static_cast<int>(n_chunks);
     f.cross_part = cross; f.cross_parts = ks * su.ns;
-    f.ba_part = ba; f.ba_parts = sb.ns;
+    if (!partial) { f.ba_part = ba; f.ba_parts = sb.ns; }
     f.d_out = d_out; f.two_s = 2.0 * a.s; f.s2 = a.s * a.s;
     f.base_sq = a.base_sq; f.cross = a.cross; f.ba_sq = a.ba_sq;
     f.round_dt = a.round_dt; f.w_norm = a.w_norm;
     f.m = a.m; f.mag_dt = a.mag_dt; f.g = a.m ? a.g : nullptr;
+    if (partial) { f.w_norm = nullptr; f.g = nullptr; f.ba_sq = nullptr; }
+    if (launches) ++*launches;
+    return launch_finish(f, st);
+}
+
+// d_in split, step 2 (after the caller's all-reduce of {G, base_sq, cross}): B [G_hi|G_lo]
+// on all SMs, then assemble / round / magnitude.  Reads no W.
+cudaError_t launch_norm_finish_tc(const NormArgs& a, Workspace* ws, cudaStream_t st,
+                                  int* launches) {
+    cudaError_t err = cudaSuccess;
+    const int64_t r = a.r, d_out = a.d_out;
+    const int64_t r_pad = (r + kBK - 1) / kBK * kBK;
+    const int64_t m_tiles = (d_out + kBM - 1) / kBM;
+    const int sms = ws_sm_count(ws);
+    FinishArgs f{};
+    f.base_part = a.base_in; f.base_parts = 1;
+    f.d_out = d_out; f.two_s = 2.0 * a.s; f.s2 = a.s * a.s;
+    f.base_sq = a.base_sq; f.cross = a.cross; f.ba_sq = a.ba_sq;
+    f.round_dt = a.round_dt; f.w_norm = a.w_norm;
+    f.m = a.m; f.mag_dt = a.mag_dt; f.g = a.m ? a.g : nullptr;
+    if (a.s != 0.0) {  // s == 0: the reference skips cross / ba_sq (factored_norm.cpp:37)
+        __nv_bfloat16* g2 = static_cast<__nv_bfloat16*>(
+            ws_get(ws, kWsGram2, size_t(r) * 2 * r_pad * sizeof(__nv_bfloat16), &err));
+        if (err != cudaSuccess) return err;
+        const Split sb = choose_split(m_tiles, r, 2 * r_pad / kBK, 1, sms);
+        float* ba = static_cast<float*>(ws_get(ws, kWsBa, size_t(sb.ns) * d_out * sizeof(float), &err));
+        if (err != cudaSuccess) return err;
+        const int64_t n = r * r_pad;
+        prof_begin("gram_split", st);
+        gram_split<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(a.gram_in, r, r_pad, g2);
+        prof_end(st);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        CUtensorMap tb, tg;
+        err = make_tmap_2d(&tb, kBF16, a.b, d_out, r, r * 2, kBK, kBM, true);
+        if (err != cudaSuccess) return err;
+        err = make_tmap_2d(&tg, kBF16, g2, r, 2 * r_pad, 2 * r_pad * 2, kBK, sb.bn, true);
+        if (err != cudaSuccess) return err;
+        TcParams p{};
+        p.M = d_out; p.N = r; p.k_total = 2 * r_pad;
+        p.kb_per_split = static_cast<int>(2 * r_pad / kBK);
+        p.n_split = sb.ns; p.bn = sb.bn; p.stages = stages_for(sb.bn);
+        p.x_kwrap = static_cast<int>(r_pad); p.chunk = 64;
+        p.Z = static_cast<const __nv_bfloat16*>(a.b); p.ldz = r;
+        p.out = ba; p.do_chain = 0;
+        p.tiles = static_cast<int>(m_tiles * sb.ns);
+        err = launch_tc(kTcRowdot, tb, tg, p, dim3(std::min(p.tiles, sms), 1), st, "ba_rowdot_tc");
+        if (err != cudaSuccess) return err;
+        if (launches) *launches += 2;
+        f.cross_part = a.cross_in; f.cross_parts = 1;
+        f.ba_part = ba; f.ba_parts = sb.ns;
+    }
     if (launches) ++*launches;
     return launch_finish(f, st);
 }

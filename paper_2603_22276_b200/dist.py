@@ -1,0 +1,92 @@
+"""Multi-GPU plumbing for the DoRA hot path.
+
+Three ways the path spreads over the GPUs of one box:
+
+* **Module sharding** (the C5 layer stack): modules are independent, so each rank runs
+  whole modules; `lpt_shards` balances them by cost (greedy longest-processing-time).
+  No data-path collective.
+* **Row split** of one module: a rank owns W / B / compose columns of a d_out block — the
+  same kernels on a row slice, no exchange.
+* **d_in split** (FSDP2 / TP-row style, the paper's stated gap): a rank
+  owns W[:, K_k] and A[:, K_k].  The factored norm needs one exchange: the Gram G, base_sq
+  and cross are sums over K, so each rank computes its slice's terms (`dfx_norm_partial`),
+  ONE all-reduce sums {G [r*r], base_sq [d_out], cross [d_out]} (0.66 MB at r=384,
+  d_out=8192), and every rank finishes locally (`dfx_norm_finish`: ba_sq = rowquad(B, G),
+  assemble, round, magnitude).
+
+The collective goes through torch.distributed (NCCL over NVLink on GPUs; gloo in the CPU
+tests).  K slices are aligned to the ChunkPlan so that each rank's base_sq chain covers
+whole chunks; with two ranks the reduced base_sq is then bitwise the reference's
+`base_sq += partial` over chunks (factored_norm.cpp:52-60).
+"""
+from __future__ import annotations
+
+import heapq
+from typing import List, Sequence, Tuple
+
+
+def module_cost(d_out: int, d_in: int, r: int, tokens: int, eb: int = 2) -> float:
+    """Relative cost of one module on B200: tensor time of the norm + HBM time of the
+    compose, in microseconds at the measured peaks (1388 TF/s sustained, 6554 GB/s)."""
+    flops = 2.0 * d_out * d_in * r + 2.0 * r * r * d_in + 4.0 * d_out * r * r
+    bytes_ = eb * (d_out * d_in + 3.0 * tokens * d_out)
+    return flops / 1388e12 * 1e6 + bytes_ / 6554e9 * 1e6
+
+
+def lpt_shards(costs: Sequence[float], n_ranks: int) -> List[List[int]]:
+    """Greedy LPT: modules in decreasing cost, each to the least-loaded rank (ties: lowest
+    rank, then lowest module index) — deterministic, within 4/3 of the optimum makespan."""
+    if n_ranks < 1:
+        raise ValueError("n_ranks must be >= 1")
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    heap = [(0.0, k) for k in range(n_ranks)]
+    shards: List[List[int]] = [[] for _ in range(n_ranks)]
+    for i in order:
+        load, k = heapq.heappop(heap)
+        shards[k].append(i)
+        heapq.heappush(heap, (load + costs[i], k))
+    for sh in shards:
+        sh.sort()
+    return shards
+
+
+def vlm32b_stack(hidden: int = 5120, mlp: int = 27648, layers: int = 64, kv_heads: int = 8,
+                 head_dim: int = 128) -> List[Tuple[str, int, int]]:
+    """The C5 inventory assumed by SURVEY sec. 8(d): 7 adapted modules per layer
+    (q, k, v, o, gate, up, down) x 64 layers = 448 (d_out, d_in) modules."""
+    kv = kv_heads * head_dim
+    per_layer = [("q", hidden, hidden), ("k", kv, hidden), ("v", kv, hidden),
+                 ("o", hidden, hidden), ("gate", mlp, hidden), ("up", mlp, hidden),
+                 ("down", hidden, mlp)]
+    return [(f"l{l}.{n}", o, i) for l in range(layers) for (n, o, i) in per_layer]
+
+
+def dsplit_bounds(d_in: int, world: int, chunk_size: int) -> List[Tuple[int, int]]:
+    """K ranges [k0, k1) per rank for the d_in split, on ChunkPlan chunk boundaries when
+    there are at least `world` chunks (whole chunks per rank), else on 64-column
+    boundaries (then base_sq is chunk-split and only tolerance-equal)."""
+    n_chunks = (d_in + chunk_size - 1) // chunk_size
+    unit = chunk_size if n_chunks >= world else 64
+    units = (d_in + unit - 1) // unit
+    out = []
+    for k in range(world):
+        u0, u1 = units * k // world, units * (k + 1) // world
+        out.append((min(u0 * unit, d_in), min(u1 * unit, d_in)))
+    return out
+
+
+def row_norm_dsplit(dfx, W_k, A_k, B, s: float, chunk_size: int, w_norm, m=None, g=None,
+                    terms=None, group=None):
+    """d_in-split factored norm on this rank: partial terms -> one all-reduce -> finish.
+    W_k / A_k are this rank's K columns (contiguous), B and m are replicated."""
+    import torch
+    import torch.distributed as tdist
+
+    d_out, r = B.shape
+    buf = torch.empty(r * r + 2 * d_out, dtype=torch.float32, device=B.device)
+    gram, base, cross = buf[: r * r], buf[r * r: r * r + d_out], buf[r * r + d_out:]
+    dfx.norm_partial(W_k, A_k, B, chunk_size, gram, base, cross)
+    if tdist.is_available() and tdist.is_initialized():
+        tdist.all_reduce(buf, op=tdist.ReduceOp.SUM, group=group)
+    dfx.norm_finish(B, gram, base, cross, s, w_norm, m=m, g=g, terms=terms)
+    return buf

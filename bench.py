@@ -39,6 +39,7 @@ UNIT = "modules/s"
 
 CONFIGS = {
     # name: d_out, d_in, r, tokens, dtype
+    "c1": dict(d_out=4096, d_in=4096, r=384, tokens=4096, dtype="fp32"),
     "c2": dict(d_out=8192, d_in=8192, r=384, tokens=4096, dtype="bf16"),
     "c3": dict(d_out=28672, d_in=8192, r=384, tokens=4096, dtype="bf16"),
     "c4r64": dict(d_out=8192, d_in=8192, r=64, tokens=4096, dtype="bf16"),

@@ -771,6 +771,125 @@ bool norm_tc_supported(int dt, int64_t d_out, int64_t d_in, int64_t r) {
 cudaError_t launch_norm_finish_tc(const NormArgs& a, Workspace* ws, cudaStream_t st,
                                   int* launches);
 
+// ------------------------------------------------------------------- planning
+// Cycle model of one persistent GEMM launch (tools/mma_micro.cu: a K=16 UMMA step costs
+// ~120 cycles for N <= 192, ~N/2 above; + a per-tile prologue/epilogue term).
+double gemm_cycles(int64_t work, int ctas, int64_t kb, int bn) {
+    if (work <= 0) return 0.0;
+    const int64_t rounds = (work + ctas - 1) / ctas;
+    return double(rounds) * (double(kb) * 4.0 * std::max(120.0, 0.5 * bn) + 2500.0);
+}
+
+// The norm's three GEMMs: U = W A^T (+ base_sq chain), G = A A^T (+ fixed-order split
+// reduction to [G_hi | G_lo]) and V = B [G_hi | G_lo].  Only U reads W; G and V depend on
+// the adapter alone.  Strategies (chosen per shape by the cycle model):
+//   kSideAll   G, reduce, V on a side stream on `side` SMs, concurrent with U
+//   kSideGram  G, reduce on the side SMs concurrent with U; V after U on all SMs
+//   kSerial    G (all SMs), reduce, U (all SMs), V (all SMs)
+enum Strategy { kSideAll = 0, kSideGram = 1, kSerial = 2 };
+
+struct UPlan {
+    bool pair;
+    Split sp;
+    int ks, kbps;
+    int64_t work;   // CTAs per K split
+    int ctas;       // CTAs launched
+    double cycles;
+};
+
+struct NormPlan {
+    Strategy strategy;
+    int side;       // side-stream SM budget (kSideAll / kSideGram)
+    UPlan u;
+    int g_ks, g_kbps, g_ctas;
+    Split sb;
+    int b_ctas;
+    double cycles;
+};
+
+UPlan plan_u(int64_t d_out, int64_t r, int64_t kb_in, int64_t chunk_blocks, int64_t n_chunks,
+             int budget) {
+    UPlan u{};
+    const int64_t m_tiles = (d_out + kBM - 1) / kBM;
+    const int64_t pm_tiles = (d_out + 2 * kBM - 1) / (2 * kBM);
+    u.pair = m_tiles >= 2 && pair_enabled() && budget >= 2;
+    const int max_ks = static_cast<int>(std::min<int64_t>(n_chunks, 8));
+    u.sp = u.pair ? choose_split(pm_tiles, r, kb_in, max_ks, budget / 2, 32)
+                  : choose_split(m_tiles, r, kb_in, max_ks, budget);
+    const int64_t chunks_per_split = (n_chunks + u.sp.ks - 1) / u.sp.ks;
+    u.kbps = static_cast<int>(chunks_per_split * chunk_blocks);
+    u.ks = static_cast<int>((kb_in + u.kbps - 1) / u.kbps);
+    u.work = (u.pair ? 2 * pm_tiles : m_tiles) * u.sp.ns;
+    u.ctas = static_cast<int>(std::min<int64_t>(u.work * u.ks, budget));
+    u.cycles = u.pair ? gemm_cycles(pm_tiles * u.sp.ns * u.ks, std::max(1, u.ctas / 2), u.kbps, u.sp.bn)
+                      : gemm_cycles(u.work * u.ks, std::max(1, u.ctas), u.kbps, u.sp.bn);
+    return u;
+}
+
+NormPlan plan_norm(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, int sms,
+                   bool need_v) {
+    const int64_t r_pad = (r + kBK - 1) / kBK * kBK;
+    const int64_t m_tiles = (d_out + kBM - 1) / kBM;
+    const int64_t kb_in = (d_in + kBK - 1) / kBK;
+    const int64_t chunk_blocks = chunk_size / kBK;
+    const int64_t n_chunks = (d_in + chunk_size - 1) / chunk_size;
+    const int nt = static_cast<int>((r + kBM - 1) / kBM);
+    const int gtiles = nt * (nt + 1) / 2;
+    const double kReduce = 12000.0;  // fixed-order split reduction kernel
+
+    auto gram = [&](int budget, int& ks, int& kbps, int& ctas) {
+        ks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(budget / gtiles, kb_in / 8)));
+        kbps = static_cast<int>((kb_in + ks - 1) / ks);
+        ks = static_cast<int>((kb_in + kbps - 1) / kbps);
+        ctas = std::min(gtiles, std::max(1, budget / ks)) * ks;
+        return gemm_cycles(int64_t(gtiles) * ks, ctas, kbps, kBM) + kReduce;
+    };
+    auto vgemm = [&](int budget, Split& sb, int& ctas) {
+        if (!need_v) { sb = {1, 1, 16}; ctas = 0; return 0.0; }
+        sb = choose_split(m_tiles, r, 2 * r_pad / kBK, 1, budget);
+        ctas = static_cast<int>(std::min<int64_t>(m_tiles * sb.ns, budget));
+        return gemm_cycles(m_tiles * sb.ns, ctas, 2 * r_pad / kBK, sb.bn);
+    };
+
+    NormPlan best{};
+    best.cycles = 1e300;
+    // serial on all SMs
+    {
+        NormPlan p{};
+        p.strategy = kSerial;
+        p.side = 0;
+        p.u = plan_u(d_out, r, kb_in, chunk_blocks, n_chunks, sms);
+        const double g = gram(sms, p.g_ks, p.g_kbps, p.g_ctas);
+        const double v = vgemm(sms, p.sb, p.b_ctas);
+        p.cycles = g + p.u.cycles + v;
+        best = p;
+    }
+    for (int side : {8, 12, 20, 28, 36, 52, 74}) {
+        if (side >= sms) break;
+        UPlan u = plan_u(d_out, r, kb_in, chunk_blocks, n_chunks, sms - side);
+        // leave exactly the SMs U does not use to the side stream
+        const int side_eff = std::max(side, sms - u.ctas) & ~1;
+        int gks, gkbps, gctas;
+        const double g = gram(side_eff, gks, gkbps, gctas);
+        for (Strategy st : {kSideAll, kSideGram}) {
+            NormPlan p{};
+            p.strategy = st;
+            p.side = side_eff;
+            p.u = u;
+            p.g_ks = gks; p.g_kbps = gkbps; p.g_ctas = gctas;
+            if (st == kSideAll) {
+                const double v = vgemm(side_eff, p.sb, p.b_ctas);
+                p.cycles = std::max(u.cycles, g + v);
+            } else {
+                const double v = vgemm(sms, p.sb, p.b_ctas);
+                p.cycles = std::max(u.cycles, g) + v;
+            }
+            if (p.cycles < best.cycles * 0.999) best = p;
+        }
+    }
+    return best;
+}
+
 cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, int* launches) {
     if (a.mode == kNormFinish) return launch_norm_finish_tc(a, ws, st, launches);
     if (!norm_tc_supported(a.dt, a.d_out, a.d_in, a.r)) return cudaErrorNotSupported;
@@ -779,140 +898,134 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
     const int64_t r = a.r, d_out = a.d_out, d_in = a.d_in;
     const int64_t r_pad = (r + kBK - 1) / kBK * kBK;
     const int64_t m_tiles = (d_out + kBM - 1) / kBM;
-    const int64_t kb_in = (d_in + kBK - 1) / kBK;
-
-    // SM budget: W A^T (the dominant GEMM, on the caller's stream) gets sms - kSide CTAs;
-    // the adapter-only chain Gram -> hi/lo -> B G runs concurrently on a side stream on
-    // the remaining kSide SMs (it does not depend on W), joined before the finisher.
-    const int sms = ws_sm_count(ws);
-    const int kMinSide = 8;
-
-    // ---------------- W A^T: cross partials + base_sq chain (main stream) --------------
-    // K splits only on ChunkPlan boundaries (each split = whole chunks)
-    const int64_t chunk_blocks = a.chunk_size / kBK;
-    const int64_t n_chunks = (d_in + a.chunk_size - 1) / a.chunk_size;
-    // 2-SM pairs (M = 256 per pair) whenever there are two row tiles to pair up
     const int64_t pm_tiles = (d_out + 2 * kBM - 1) / (2 * kBM);
-    const bool use_pair = m_tiles >= 2 && pair_enabled();
-    const Split su = use_pair
-        ? choose_split(pm_tiles, r, kb_in, static_cast<int>(std::min<int64_t>(n_chunks, 8)),
-                       (sms - kMinSide) / 2, 32)
-        : choose_split(m_tiles, r, kb_in, static_cast<int>(std::min<int64_t>(n_chunks, 8)),
-                       sms - kMinSide);
-    const int64_t u_work = (use_pair ? 2 * pm_tiles : m_tiles) * su.ns;  // CTAs per K split
+    const int64_t n_chunks = (d_in + a.chunk_size - 1) / a.chunk_size;
+    const int sms = ws_sm_count(ws);
 
-    const int64_t chunks_per_split = (n_chunks + su.ks - 1) / su.ks;
-    const int kbps = static_cast<int>(chunks_per_split * chunk_blocks);
-    const int ks = static_cast<int>((kb_in + kbps - 1) / kbps);
-    // the U GEMM takes one round of CTAs if it fits, the side chain the remaining SMs
-    const int main_ctas = static_cast<int>(std::min<int64_t>(u_work * ks, sms - kMinSide));
-    const int kSide = std::max(kMinSide, sms - main_ctas);
+    const NormPlan plan = plan_norm(d_out, d_in, r, a.chunk_size, sms, !partial);
+    const UPlan& u = plan.u;
+    const bool forked = plan.strategy != kSerial;
+    // side kernels occupy whole TPCs beside the 2-SM U pairs
+    const bool tpc = forked && u.pair;
+
     float* cross = static_cast<float*>(
-        ws_get(ws, kWsCross, size_t(ks) * su.ns * d_out * sizeof(float), &err));
+        ws_get(ws, kWsCross, size_t(u.ks) * u.sp.ns * d_out * sizeof(float), &err));
     if (err != cudaSuccess) return err;
     float* base = static_cast<float*>(
         ws_get(ws, kWsBase, size_t(n_chunks) * d_out * sizeof(float), &err));
     if (err != cudaSuccess) return err;
-
-    // adapter-side buffers
     const int nt = static_cast<int>((r + kBM - 1) / kBM);
     const int gtiles = nt * (nt + 1) / 2;
-    int g_ks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kSide / gtiles, kb_in / 8)));
-    const int g_kbps = static_cast<int>((kb_in + g_ks - 1) / g_ks);
-    g_ks = static_cast<int>((kb_in + g_kbps - 1) / g_kbps);
     float* gpart = static_cast<float*>(
-        ws_get(ws, kWsGramPart, size_t(g_ks) * gtiles * kBM * kBM * sizeof(float), &err));
+        ws_get(ws, kWsGramPart, size_t(plan.g_ks) * gtiles * kBM * kBM * sizeof(float), &err));
     if (err != cudaSuccess) return err;
     __nv_bfloat16* g2 = static_cast<__nv_bfloat16*>(
         ws_get(ws, kWsGram2, size_t(r) * 2 * r_pad * sizeof(__nv_bfloat16), &err));
     if (err != cudaSuccess) return err;
-    const Split sb = choose_split(m_tiles, r, 2 * r_pad / kBK, 1, kSide);
-    float* ba = static_cast<float*>(ws_get(ws, kWsBa, size_t(sb.ns) * d_out * sizeof(float), &err));
+    float* ba = static_cast<float*>(
+        ws_get(ws, kWsBa, size_t(plan.sb.ns) * d_out * sizeof(float), &err));
     if (err != cudaSuccess) return err;
 
-    cudaStream_t side = ws_side_stream(ws, &err);
-    if (err != cudaSuccess) return err;
-    cudaEvent_t ev_fork = ws_event(ws, 0, &err), ev_join = ws_event(ws, 1, &err);
-    if (err != cudaSuccess) return err;
-    if ((err = cudaEventRecord(ev_fork, st)) != cudaSuccess) return err;
-    if ((err = cudaStreamWaitEvent(side, ev_fork, 0)) != cudaSuccess) return err;
+    cudaStream_t side = st;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (forked) {
+        side = ws_side_stream(ws, &err);
+        if (err != cudaSuccess) return err;
+        ev_fork = ws_event(ws, 0, &err);
+        ev_join = ws_event(ws, 1, &err);
+        if (err != cudaSuccess) return err;
+        if ((err = cudaEventRecord(ev_fork, st)) != cudaSuccess) return err;
+        if ((err = cudaStreamWaitEvent(side, ev_fork, 0)) != cudaSuccess) return err;
+    }
 
-    {
+    auto launch_u = [&]() -> cudaError_t {
         CUtensorMap tw, ta;
-        err = make_tmap_2d(&tw, kBF16, a.w, d_out, d_in, d_in * 2, kBK, kBM, true);
-        if (err != cudaSuccess) return err;
-        err = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, su.bn, true);
-        if (err != cudaSuccess) return err;
+        cudaError_t e = make_tmap_2d(&tw, kBF16, a.w, d_out, d_in, d_in * 2, kBK, kBM, true);
+        if (e != cudaSuccess) return e;
         TcParams p{};
-        p.M = d_out; p.N = r; p.k_total = d_in; p.kb_per_split = kbps;
-        p.n_split = su.ns; p.bn = su.bn; p.stages = stages_for(su.bn);
+        p.M = d_out; p.N = r; p.k_total = d_in; p.kb_per_split = u.kbps;
+        p.n_split = u.sp.ns; p.bn = u.sp.bn;
         p.x_kwrap = 0; p.chunk = a.chunk_size;
         p.Z = static_cast<const __nv_bfloat16*>(a.b); p.ldz = r;
         p.out = cross; p.base_out = base; p.do_chain = 1;
-        if (use_pair) {
+        if (u.pair) {
             // A box = half of the pair's BN rows (each CTA of the pair loads its half)
-            err = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, su.bn / 2, true);
-            if (err != cudaSuccess) return err;
-            p.stages = stages_for_pair(su.bn);
-            p.tiles = static_cast<int>(pm_tiles * su.ns);
-            const int pairs = std::min<int>(p.tiles, std::max(1, main_ctas / (2 * ks)));
-            err = launch_tc_pair(tw, ta, p, pairs, ks, st, "u_rowdot_tc");
+            e = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, u.sp.bn / 2, true);
+            if (e != cudaSuccess) return e;
+            p.stages = stages_for_pair(u.sp.bn);
+            p.tiles = static_cast<int>(pm_tiles * u.sp.ns);
+            const int pairs = std::min<int>(p.tiles, std::max(1, u.ctas / (2 * u.ks)));
+            e = launch_tc_pair(tw, ta, p, pairs, u.ks, st, "u_rowdot_tc");
         } else {
-            p.tiles = static_cast<int>(m_tiles * su.ns);
-            const int gx = std::min<int>(p.tiles, std::max(1, main_ctas / ks));
-            err = launch_tc(kTcRowdot, tw, ta, p, dim3(gx, ks), st, "u_rowdot_tc");
+            e = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, u.sp.bn, true);
+            if (e != cudaSuccess) return e;
+            p.stages = stages_for(u.sp.bn);
+            p.tiles = static_cast<int>(m_tiles * u.sp.ns);
+            const int gx = std::min<int>(p.tiles, std::max(1, u.ctas / u.ks));
+            e = launch_tc(kTcRowdot, tw, ta, p, dim3(gx, u.ks), st, "u_rowdot_tc");
         }
-        if (err != cudaSuccess) return err;
-        if (launches) ++*launches;
-    }
-
-    // ---------------- side stream: G = A A^T -> [G_hi | G_lo] -> ba_sq partials --------
-    {
+        if (e == cudaSuccess && launches) ++*launches;
+        return e;
+    };
+    auto launch_gram = [&](cudaStream_t gs) -> cudaError_t {
         CUtensorMap ta;
-        err = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, kBM, true);
-        if (err != cudaSuccess) return err;
+        cudaError_t e = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, kBM, true);
+        if (e != cudaSuccess) return e;
         TcParams p{};
-        p.M = r; p.N = r; p.k_total = d_in; p.kb_per_split = g_kbps; p.n_split = 1;
+        p.M = r; p.N = r; p.k_total = d_in; p.kb_per_split = plan.g_kbps; p.n_split = 1;
         p.bn = kBM; p.stages = stages_for(kBM); p.chunk = a.chunk_size;
         p.out = gpart; p.gram_nt = nt; p.tiles = gtiles;
-        const int gx = std::min(gtiles, std::max(1, kSide / g_ks));
-        err = launch_tc(kTcStore, ta, ta, p, dim3(gx, g_ks), side, "gram_tc", use_pair);
-        if (err != cudaSuccess) return err;
+        const int gx = std::min(gtiles, std::max(1, plan.g_ctas / plan.g_ks));
+        e = launch_tc(kTcStore, ta, ta, p, dim3(gx, plan.g_ks), gs, "gram_tc", tpc && gs != st);
+        if (e != cudaSuccess) return e;
         const int64_t n = r * r_pad;
-        prof_begin("gram_reduce", side);
-        gram_reduce<<<static_cast<unsigned>((n + 255) / 256), 256, 0, side>>>(
-            gpart, g_ks, nt, r, r_pad, partial ? nullptr : g2, partial ? a.gram_out : nullptr);
-        prof_end(side);
-        err = cudaGetLastError();
-        if (err != cudaSuccess) return err;
+        prof_begin("gram_reduce", gs);
+        gram_reduce<<<static_cast<unsigned>((n + 255) / 256), 256, 0, gs>>>(
+            gpart, plan.g_ks, nt, r, r_pad, partial ? nullptr : g2, partial ? a.gram_out : nullptr);
+        prof_end(gs);
         if (launches) *launches += 2;
-    }
-    if (!partial) {
+        return cudaGetLastError();
+    };
+    auto launch_v = [&](cudaStream_t vs) -> cudaError_t {
         CUtensorMap tb, tg;
-        err = make_tmap_2d(&tb, kBF16, a.b, d_out, r, r * 2, kBK, kBM, true);
-        if (err != cudaSuccess) return err;
-        err = make_tmap_2d(&tg, kBF16, g2, r, 2 * r_pad, 2 * r_pad * 2, kBK, sb.bn, true);
-        if (err != cudaSuccess) return err;
+        cudaError_t e = make_tmap_2d(&tb, kBF16, a.b, d_out, r, r * 2, kBK, kBM, true);
+        if (e != cudaSuccess) return e;
+        e = make_tmap_2d(&tg, kBF16, g2, r, 2 * r_pad, 2 * r_pad * 2, kBK, plan.sb.bn, true);
+        if (e != cudaSuccess) return e;
         TcParams p{};
         p.M = d_out; p.N = r; p.k_total = 2 * r_pad;
         p.kb_per_split = static_cast<int>(2 * r_pad / kBK);
-        p.n_split = sb.ns; p.bn = sb.bn; p.stages = stages_for(sb.bn);
+        p.n_split = plan.sb.ns; p.bn = plan.sb.bn; p.stages = stages_for(plan.sb.bn);
         p.x_kwrap = static_cast<int>(r_pad); p.chunk = a.chunk_size;
         p.Z = static_cast<const __nv_bfloat16*>(a.b); p.ldz = r;
         p.out = ba; p.do_chain = 0;
-        p.tiles = static_cast<int>(m_tiles * sb.ns);
-        const int gx = std::min(p.tiles, kSide);
-        err = launch_tc(kTcRowdot, tb, tg, p, dim3(gx, 1), side, "ba_rowdot_tc", use_pair);
-        if (err != cudaSuccess) return err;
-        if (launches) ++*launches;
+        p.tiles = static_cast<int>(m_tiles * plan.sb.ns);
+        e = launch_tc(kTcRowdot, tb, tg, p, dim3(std::max(1, plan.b_ctas), 1), vs, "ba_rowdot_tc",
+                      tpc && vs != st);
+        if (e == cudaSuccess && launches) ++*launches;
+        return e;
+    };
+
+    if (plan.strategy == kSerial) {
+        if ((err = launch_gram(st)) != cudaSuccess) return err;
+        if ((err = launch_u()) != cudaSuccess) return err;
+        if (!partial && (err = launch_v(st)) != cudaSuccess) return err;
+    } else {
+        // U first on the caller's stream (it claims its SMs), the adapter chain beside it
+        if ((err = launch_u()) != cudaSuccess) return err;
+        if ((err = launch_gram(side)) != cudaSuccess) return err;
+        if (plan.strategy == kSideAll && !partial && (err = launch_v(side)) != cudaSuccess)
+            return err;
+        if ((err = cudaEventRecord(ev_join, side)) != cudaSuccess) return err;
+        if ((err = cudaStreamWaitEvent(st, ev_join, 0)) != cudaSuccess) return err;
+        if (plan.strategy == kSideGram && !partial && (err = launch_v(st)) != cudaSuccess)
+            return err;
     }
-    if ((err = cudaEventRecord(ev_join, side)) != cudaSuccess) return err;
-    if ((err = cudaStreamWaitEvent(st, ev_join, 0)) != cudaSuccess) return err;
 
     FinishArgs f{};
     f.base_part = base; f.base_parts = static_cast<int>(n_chunks);
-    f.cross_part = cross; f.cross_parts = ks * su.ns;
-    if (!partial) { f.ba_part = ba; f.ba_parts = sb.ns; }
+    f.cross_part = cross; f.cross_parts = u.ks * u.sp.ns;
+    if (!partial) { f.ba_part = ba; f.ba_parts = plan.sb.ns; }
     f.d_out = d_out; f.two_s = 2.0 * a.s; f.s2 = a.s * a.s;
     f.base_sq = a.base_sq; f.cross = a.cross; f.ba_sq = a.ba_sq;
     f.round_dt = a.round_dt; f.w_norm = a.w_norm;

@@ -287,11 +287,26 @@ __global__ void __launch_bounds__(SerialCfg<T>::kThreads, 1)
             const T* pi = reinterpret_cast<const T*>(s_in + s * C::kStageBytes) + jc;
             const int64_t rem = rows - int64_t(it) * C::kRB;
             const int nr = rem < C::kRB ? static_cast<int>(rem) : C::kRB;
-#pragma unroll 8
-            for (int i = 0; i < nr; ++i) {
-                const float p = __fmul_rn(Elem<T>::to_f(py[i * C::kSC]),
-                                          Elem<T>::to_f(pi[i * C::kSC]));
-                acc = __fadd_rn(acc, p);
+            if (nr == C::kRB) {
+                // Full stage: load a batch of 16 rows into registers, form the 16
+                // (independent) products, then run the dependent adds in row order, so
+                // shared-memory latency is paid once per batch, not once per row.
+#pragma unroll
+                for (int i0 = 0; i0 < C::kRB; i0 += 16) {
+                    float p[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u)
+                        p[u] = __fmul_rn(Elem<T>::to_f(py[(i0 + u) * C::kSC]),
+                                         Elem<T>::to_f(pi[(i0 + u) * C::kSC]));
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) acc = __fadd_rn(acc, p[u]);
+                }
+            } else {
+                for (int i = 0; i < nr; ++i) {
+                    const float p = __fmul_rn(Elem<T>::to_f(py[i * C::kSC]),
+                                              Elem<T>::to_f(pi[i * C::kSC]));
+                    acc = __fadd_rn(acc, p);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);

@@ -1,2 +1,5 @@
-for cfg in "" "DFX_NORM_BA=after"; do
-  for st in norm module; do echo "== $cfg $st"; env $cfg timeout 120 python bench.py --steps 2000 --e2e-steps 0 --no-cpu-baseline --prof-steps 2 --stage $st 2>&1 | grep -o 'timed.*'; done; done
+#!/bin/bash
+O=gpurun_out/exp.txt; : > $O
+E="timeout 60 python scripts/exp_kernels.py"
+for sv in 8 7 6 4 2; do DFX_BWD_SV=$sv $E --what bwd --tag sv$sv >> $O 2>&1; done
+for sv in 8 7 4; do DFX_BWD_SV=$sv $E --config c1 --what bwd --tag sv$sv >> $O 2>&1; done

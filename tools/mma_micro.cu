@@ -9,7 +9,7 @@
 using namespace dfx;
 
 template <int kPair>
-__global__ void __launch_bounds__(128, 1) mma_loop(int n, int iters, long long* cycles) {
+__global__ void __launch_bounds__(128, 1) mma_loop(int n, int iters, long long* cycles, int inter) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sa = smem;              // 128 rows x 128 B (one K=64 block of A)
@@ -18,7 +18,7 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int n, int iters, long long* 
     uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 8);
     for (int i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
     if (threadIdx.x == 0) { for (int i = 0; i < 8; ++i) mbar_init(&bar[i], 1); fence_mbar_init(); }
-    if (threadIdx.x / 32 == 0) { if (kPair) tmem_alloc_pair<256>(slot); else tmem_alloc<256>(slot); }
+    if (threadIdx.x / 32 == 0) { if (kPair) tmem_alloc_pair<512>(slot); else tmem_alloc<512>(slot); }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before(); __syncthreads(); if (kPair) cluster_sync(); tc_fence_after();
     const uint32_t tmem = *slot;
@@ -32,8 +32,9 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int n, int iters, long long* 
             const int s = it & 7;
             if (it >= 8) { mbar_wait(&bar[s], ph[s]); ph[s] ^= 1; }
             for (int k = 0; k < 4; ++k) {
-                if (kPair) umma_f16_pair(tmem, umma_desc_k_sw128(a + k * 32), umma_desc_k_sw128(b + k * 32), idesc, 1);
-                else umma_f16(tmem, umma_desc_k_sw128(a + k * 32), umma_desc_k_sw128(b + k * 32), idesc, 1);
+                const uint32_t acc = tmem + (inter ? uint32_t(k & 1) * uint32_t(n) : 0u);
+                if (kPair) umma_f16_pair(acc, umma_desc_k_sw128(a + k * 32), umma_desc_k_sw128(b + k * 32), idesc, 1);
+                else umma_f16(acc, umma_desc_k_sw128(a + k * 32), umma_desc_k_sw128(b + k * 32), idesc, 1);
             }
             if (kPair) umma_commit_pair_mc(&bar[s], 0x1); else umma_commit(&bar[s]);
         }
@@ -41,7 +42,7 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int n, int iters, long long* 
         cycles[blockIdx.x] = clock64() - t0;
     }
     tc_fence_before(); __syncthreads(); if (kPair) cluster_sync();
-    if (threadIdx.x / 32 == 0) { tc_fence_after(); if (kPair) tmem_dealloc_pair<256>(tmem); else tmem_dealloc<256>(tmem); }
+    if (threadIdx.x / 32 == 0) { tc_fence_after(); if (kPair) tmem_dealloc_pair<512>(tmem); else tmem_dealloc<512>(tmem); }
 }
 
 int main() {
@@ -50,7 +51,7 @@ int main() {
     const int iters = 4000, smem = 16384 + 32768 + 2048;
     cudaFuncSetAttribute(mma_loop<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(mma_loop<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int pair = 0; pair < 2; ++pair) for (int n : {64, 128, 192, 256}) {
+    for (int inter = 0; inter < 2; ++inter) for (int pair = 0; pair < 2; ++pair) for (int n : {64, 128, 192, 256}) {
         const int grid = pair ? (sms / 2) * 2 : sms;
         cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
         cudaLaunchConfig_t cfg = {}; cfg.gridDim = dim3(grid); cfg.blockDim = dim3(128); cfg.dynamicSmemBytes = smem;
@@ -58,7 +59,7 @@ int main() {
         cfg.attrs = at; cfg.numAttrs = 1;
         for (int rep = 0; rep < 2; ++rep) {
             cudaEventRecord(e0);
-            cudaError_t err = pair ? cudaLaunchKernelEx(&cfg, mma_loop<1>, n, iters, d) : cudaLaunchKernelEx(&cfg, mma_loop<0>, n, iters, d);
+            cudaError_t err = pair ? cudaLaunchKernelEx(&cfg, mma_loop<1>, n, iters, d, inter) : cudaLaunchKernelEx(&cfg, mma_loop<0>, n, iters, d, inter);
             cudaEventRecord(e1); cudaEventSynchronize(e1);
             if (err != cudaSuccess || cudaGetLastError() != cudaSuccess) { printf("launch failed %s\n", cudaGetErrorString(err)); return 1; }
         }
@@ -66,8 +67,8 @@ int main() {
         long long h[512]; cudaMemcpy(h, d, sizeof(long long) * 512, cudaMemcpyDeviceToHost);
         const double macs_per_sm = double(iters) * 4 * 128 * n * 16;   // per SM (M=128 rows each)
         const long long cyc = h[0];
-        printf("%s M=%d N=%3d: %.1f us, %lld cycles on CTA0 -> %.0f MAC/cycle/SM, %.0f TFLOP/s chip\n",
-               pair ? "2-SM" : "1-SM", pair ? 256 : 128, n, ms * 1e3, cyc, macs_per_sm / cyc,
+        printf("%s%s M=%d N=%3d: %.1f us, %lld cycles on CTA0 -> %.0f MAC/cycle/SM, %.0f TFLOP/s chip\n",
+               inter ? "2acc " : "", pair ? "2-SM" : "1-SM", pair ? 256 : 128, n, ms * 1e3, cyc, macs_per_sm / cyc,
                2.0 * macs_per_sm * (pair ? grid : grid) / (ms * 1e-3) / 1e12);
     }
     return 0;

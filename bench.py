@@ -1,23 +1,29 @@
 #!/usr/bin/env python
 """bench.py — DoRA modules/s on B200 (BASELINE.json metric), one JSON line on rank 0.
 
-Workload (BASELINE.json configs[1]): one DoRA module =
-  dfx_row_norm   (factored ||W + sBA||_row: Gram, bf16 hi/lo B.G, W.A^T + base_sq chain,
-                  assemble, dtype rounding, magnitude g = m / max(norm, eps))
-  dfx_compose_fwd (delta = (g-1)*base + g*s*lora over tokens=4096 rows)
-at d_out = d_in = 8192, r = 384, bf16, s = 2/sqrt(r).  A step processes one module.
+Workload (BASELINE.json configs[1]: "single module d_out=d_in=8192 r=384 bf16,
+tokens=4096 compose fwd+bwd"): one step = one DoRA module TRAINING
+step of the hot path,
+  dfx_row_norm    factored ||W + sBA||_row (Gram, bf16 hi/lo B.G, W.A^T + base_sq chain,
+                  assemble, dtype rounding) and the magnitude g = m / max(norm, eps)
+  dfx_compose_fwd dual output: delta = (g-1)*base + g*s*lora and inner = s*lora + base
+  dfx_compose_bwd d_lora = g*s*dY, d_base = (g-1)*dY and d_mag = sum_rows(dY*inner)/norm
+at d_out = d_in = 8192, r = 384, bf16, tokens = 4096, s = 2/sqrt(r).  The inference
+module (row_norm + plain compose_fwd) is reported beside it under "variants".
 Synthetic data (seeded torch.randn on device; m = ||W+sBA|| * (1 + N(0, 0.0015)) so
-g ~ 1 as in the paper's regime).  Inputs are larger than L2 (W 128 MiB + base/lora
-128 MiB per module) and NBUF module buffer sets rotate, so every step reads cold HBM.
+g ~ 1 as in the paper's regime).  Inputs are larger than L2 (W 128 MiB + 5 activation
+tensors of 64 MiB per module) and NBUF module buffer sets rotate, so every step reads
+cold HBM.
 
-Timed region: K steps replayed as CUDA graphs (one per buffer set), CUDA events on the
-launching stream, barrier + synchronize on both sides, max over ranks.  A second pass
-with the C ABI's per-kernel event profiling (dfx_profile_*) gives the live per-kernel
-durations behind `roofline`.  `e2e` goes through the host-buffer entry point
-dfx_module_fwd_host (pinned host -> HBM -> kernels -> host).  `cpu_baseline` times the
-reference's own C++ (oracle/_ref) on this host's cores on a bounded sample.
+Timed region: K steps replayed as CUDA graphs (modules software-pipelined on two
+streams), CUDA events on the launching stream, barrier + synchronize on both sides, max
+over ranks.  A second pass with the C ABI's per-kernel event profiling (dfx_profile_*)
+gives the live per-kernel durations behind `roofline`.  `e2e` goes through the
+host-buffer entry point dfx_module_train_host (pinned host -> HBM -> kernels -> host).
+`cpu_baseline` times the reference's own C++ (oracle/_ref) on this host's cores on a
+bounded sample.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--mode infer]
 Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N  (modules shard across ranks:
 weak scaling, no data-path collective).
 """
@@ -71,6 +77,8 @@ def algorithmic(cfg):
         "gram_reduce": ("hbm", 0.0, 8.0 * r * r),
         "finish": ("hbm", 0.0, 4.0 * 5 * d_out),
         "compose_fwd": ("hbm", 0.0, 3.0 * eb * rows * d_out + 4.0 * d_out),
+        "compose_fwd_dual": ("hbm", 0.0, 4.0 * eb * rows * d_out + 4.0 * d_out),
+        "compose_bwd_dmag": ("hbm", 0.0, 4.0 * eb * rows * d_out + 12.0 * d_out),
         "norm_total": ("tensor", 2.0 * d_out * d_in * r + 2.0 * r * r * d_in + 2.0 * d_out * r * r,
                        eb * (d_out * d_in + r * d_in + d_out * r) + 4.0 * d_out),
     }
@@ -131,15 +139,17 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------- CPU reference
-def cpu_reference_rate(cfg, cores, rounds=1, warm=0, log=None):
+def cpu_reference_rate(cfg, cores, mode="train", rounds=1, warm=0, log=None):
     """The reference's own C++ (oracle/_ref/libdfx_ref.so, compiled from the reference
     sources) on this host.  The reference is single-threaded per call, so all cores run
     independent module samples concurrently (as its own suites do, suites.cpp:49-65).
 
-    A full C2 module costs ~35 s on one core, so each thread runs a bounded sample:
-    factored_row_norm on NS W-rows (full A, full d_in; Gram cost included) + fused_compose
-    on CT token rows.  A single-core calibration separates the fixed (Gram) cost from the
-    per-row and per-token costs, which converts a sample into module-equivalents:
+    A full C2 module costs ~20-40 s on one core, so each thread runs a bounded sample:
+    factored_row_norm on NS W-rows (full A, full d_in; Gram cost included) + the compose
+    on CT token rows (train: dual_output_compose + compose_backward with the magnitude
+    gradient; infer: fused_compose).  A single-core calibration separates the fixed
+    (Gram) cost from the per-row and per-token costs, which converts a sample into
+    module-equivalents:
         t_module = t_fixed + d_out * t_row + (tokens / CT) * t_compose(CT)
     Returns (modules/s, details)."""
     import numpy as np
@@ -164,7 +174,9 @@ def cpu_reference_rate(cfg, cores, rounds=1, warm=0, log=None):
     Bn = rnd(rng.standard_normal((NS2, r)))
     base = rnd(rng.standard_normal((CT, d_out)))
     lora = rnd(rng.standard_normal((CT, d_out)))
+    dy = rnd(rng.standard_normal((CT, d_out)))
     g = np.array([R.round_to_dtype(v, dt) for v in 1.0 + 0.0015 * rng.standard_normal(d_out)])
+    wn = np.array([R.round_to_dtype(v, dt) for v in 90.0 + rng.standard_normal(d_out)])
     cs, _ = R.plan_chunks(d_out, d_in)   # the full module's chunk plan
 
     def norm_sample(n):
@@ -172,18 +184,25 @@ def cpu_reference_rate(cfg, cores, rounds=1, warm=0, log=None):
         return R.last_call_s()
 
     def compose_sample():
-        R.compose(1, dt, base, lora, g, s)
-        return R.last_call_s()
+        if mode == "infer":
+            R.compose(1, dt, base, lora, g, s)
+            return R.last_call_s()
+        _, inner = R.compose(2, dt, base, lora, g, s, need_inner=True)
+        t = R.last_call_s()
+        R.compose_bwd(dt, dy, g, s, inner=inner, w_norm=wn, mag_grad=True)
+        return t + R.last_call_s()
 
-    t1 = norm_sample(NS1)
-    t2 = norm_sample(NS2)
+    norm_sample(NS1)                     # warm caches / page in A before calibrating
+    compose_sample()
+    t1 = min(norm_sample(NS1) for _ in range(2))
+    t2 = min(norm_sample(NS2) for _ in range(2))
     t_row = max((t2 - t1) / (NS2 - NS1), 1e-9)
     t_fixed = max(t1 - NS1 * t_row, 0.0)
-    t_c = compose_sample()
+    t_c = min(compose_sample() for _ in range(2))
     t_module = t_fixed + d_out * t_row + (tokens / CT) * t_c
     sample_equiv = (t_fixed + NS2 * t_row + t_c) / t_module
     if log:
-        log(f"cpu ref calibration: fixed {t_fixed:.3f}s row {t_row * 1e3:.3f}ms "
+        log(f"cpu ref calibration ({mode}): fixed {t_fixed:.3f}s row {t_row * 1e3:.3f}ms "
             f"compose({CT}) {t_c:.3f}s -> {t_module:.1f}s/module/core")
 
     def worker(out, i):
@@ -202,11 +221,13 @@ def cpu_reference_rate(cfg, cores, rounds=1, warm=0, log=None):
         if k >= warm:
             rates.append(cores * sample_equiv / wall)
     rate = sorted(rates)[len(rates) // 2]
+    what = ("dual_output_compose + compose_backward (mag_grad)" if mode == "train"
+            else "fused_compose")
     return rate, {
         "t_module_1core_s": t_module, "t_fixed_s": t_fixed, "t_row_ms": t_row * 1e3,
         "t_compose_per_token_us": t_c / CT * 1e6, "rounds": rounds,
         "sample": (f"per thread: reference factored_row_norm on {NS2} of {d_out} W rows (full "
-                   f"d_in={d_in}, r={r}, Gram included) + fused_compose on {CT} of {tokens} "
+                   f"d_in={d_in}, r={r}, Gram included) + {what} on {CT} of {tokens} "
                    f"tokens; {cores} threads concurrently; converted to modules via a 1-core "
                    f"calibration t_module = t_fixed + d_out*t_row + tokens/{CT}*t_compose "
                    f"= {t_module:.1f} s"),
@@ -241,100 +262,126 @@ def run_gpu(args, rank, world, local_rank, dist):
     gen.manual_seed(20261017 + rank)
     sets = []
     for i in range(nbuf):
-        W = torch.randn(d_out, d_in, device=dev, generator=gen).to(tdt)
-        A = torch.randn(r, d_in, device=dev, generator=gen).to(tdt)
-        B = torch.randn(d_out, r, device=dev, generator=gen).to(tdt)
-        base = torch.randn(rows, d_out, device=dev, generator=gen).to(tdt)
-        lora = torch.randn(rows, d_out, device=dev, generator=gen).to(tdt)
-        wn = torch.empty(d_out, device=dev)
-        g = torch.empty(d_out, device=dev)
-        delta = torch.empty_like(base)
-        dfx.row_norm(W, A, B, s, cs, wn)
-        m = (wn * (1.0 + 0.0015 * torch.randn(d_out, device=dev, generator=gen))).contiguous()
-        sets.append(dict(W=W, A=A, B=B, base=base, lora=lora, wn=wn, g=g, m=m, delta=delta))
+        rnd = lambda *shape: torch.randn(*shape, device=dev, generator=gen).to(tdt)
+        b = dict(W=rnd(d_out, d_in), A=rnd(r, d_in), B=rnd(d_out, r), base=rnd(rows, d_out),
+                 lora=rnd(rows, d_out), dy=rnd(rows, d_out))
+        b.update(wn=torch.empty(d_out, device=dev), g=torch.empty(d_out, device=dev),
+                 dm=torch.empty(d_out, device=dev))
+        for k in ("delta", "inner", "dl", "db"):
+            b[k] = torch.empty_like(b["base"])
+        dfx.row_norm(b["W"], b["A"], b["B"], s, cs, b["wn"])
+        b["m"] = (b["wn"] * (1.0 + 0.0015 * torch.randn(d_out, device=dev, generator=gen))).contiguous()
+        sets.append(b)
     torch.cuda.synchronize()
 
-    def step(b):
-        # --stage isolates one half of the module for analysis (the headline is "module")
-        if args.stage in ("module", "norm"):
-            dfx.row_norm(b["W"], b["A"], b["B"], s, cs, b["wn"], m=b["m"], g=b["g"])
-        if args.stage in ("module", "compose"):
-            dfx.compose_fwd(b["base"], b["lora"], b["g"], s, b["delta"])
+    def norm(b, st=None):
+        dfx.row_norm(b["W"], b["A"], b["B"], s, cs, b["wn"], m=b["m"], g=b["g"], stream=st)
+
+    def compose(b, mode, st=None):
+        if mode == "infer":
+            dfx.compose_fwd(b["base"], b["lora"], b["g"], s, b["delta"], stream=st)
+        else:
+            dfx.compose_fwd(b["base"], b["lora"], b["g"], s, b["delta"], b["inner"], stream=st)
+            dfx.compose_bwd(b["dy"], b["g"], s, b["dl"], b["db"], inner=b["inner"], w_norm=b["wn"],
+                            d_mag=b["dm"], stream=st)
+
+    def step(b, mode):
+        norm(b)
+        compose(b, mode)
 
     stream = torch.cuda.Stream(device=dev)
+    side = torch.cuda.Stream(device=dev)
+
+    def build_graphs(mode):
+        """Modules are independent, so a graph holds npipe consecutive modules software-
+        pipelined on two streams: module i's compose (HBM-bound) runs on stream B beside
+        module i+1's row norm (tensor-bound) on stream A.  Edges: compose i after norm i
+        (it reads g_i, w_norm_i); norm i+nbuf after compose i (it rewrites set i % nbuf)."""
+        npipe = args.pipeline if (args.pipeline > 1 and args.steps % args.pipeline == 0) else 1
+        graphs = []
+        if npipe > 1:
+            sA, sB = stream.cuda_stream, side.cuda_stream
+            ev_norm = [torch.cuda.Event() for _ in range(npipe)]
+            ev_comp = [torch.cuda.Event() for _ in range(npipe)]
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph, stream=stream):
+                for i in range(npipe):
+                    b = sets[i % nbuf]
+                    if i >= nbuf:
+                        stream.wait_event(ev_comp[i - nbuf])
+                    norm(b, sA)
+                    ev_norm[i].record(stream)
+                    side.wait_event(ev_norm[i])
+                    compose(b, mode, sB)
+                    ev_comp[i].record(side)
+                stream.wait_event(ev_comp[npipe - 1])
+            graphs.append(gph)
+        else:
+            for b in sets:
+                gph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gph, stream=stream):
+                    step(b, mode)
+                graphs.append(gph)
+        torch.cuda.synchronize()
+        return graphs, npipe
+
+    def timed(mode, steps, warmup, clocks=None):
+        graphs, npipe = build_graphs(mode)
+        nrep = len(graphs)
+        with torch.cuda.stream(stream):
+            for k in range((warmup + npipe - 1) // npipe):
+                graphs[k % nrep].replay()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        import contextlib
+        with (clocks if clocks is not None else contextlib.nullcontext()):
+            with torch.cuda.stream(stream):
+                ev0.record(stream)
+                for k in range(steps // npipe):
+                    graphs[k % nrep].replay()
+                ev1.record(stream)
+            torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ms = ev0.elapsed_time(ev1)
+        if dist:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, npipe
+
+    # warm each path eagerly once, count this library's kernel launches per step
     with torch.cuda.stream(stream):
         for i in range(max(2, nbuf)):
-            step(sets[i % nbuf])
+            step(sets[i % nbuf], args.mode)
     torch.cuda.synchronize()
     launches_before = dfx.launches
     with torch.cuda.stream(stream):
-        step(sets[0])
+        step(sets[0], args.mode)
     torch.cuda.synchronize()
     launches_per_step = dfx.launches - launches_before
 
-    # ---- capture the module stream as CUDA graphs
-    # Modules are independent, so a graph holds npipe consecutive modules software-pipelined
-    # on two streams: module i's compose (HBM-bound, no shared memory) runs on stream B
-    # beside module i+1's row norm (tensor-bound) on stream A.  Explicit edges: compose i
-    # after norm i (it reads g_i); norm i+nbuf after compose i (it rewrites buffer set
-    # i % nbuf's g).  --no-pipeline captures one module per graph, strictly serial.
-    side = torch.cuda.Stream(device=dev)
-    npipe = args.pipeline if (args.pipeline > 1 and args.stage == "module"
-                          and args.steps % args.pipeline == 0) else 1
-    graphs = []
-    if npipe > 1:
-        sA, sB = stream.cuda_stream, side.cuda_stream
-        ev_norm = [torch.cuda.Event() for _ in range(npipe)]
-        ev_comp = [torch.cuda.Event() for _ in range(npipe)]
-        gph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gph, stream=stream):
-            for i in range(npipe):
-                b = sets[i % nbuf]
-                if i >= nbuf:
-                    stream.wait_event(ev_comp[i - nbuf])
-                dfx.row_norm(b["W"], b["A"], b["B"], s, cs, b["wn"], m=b["m"], g=b["g"], stream=sA)
-                ev_norm[i].record(stream)
-                side.wait_event(ev_norm[i])
-                dfx.compose_fwd(b["base"], b["lora"], b["g"], s, b["delta"], stream=sB)
-                ev_comp[i].record(side)
-            stream.wait_event(ev_comp[npipe - 1])
-        graphs.append(gph)
-    else:
-        for b in sets:
-            gph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gph, stream=stream):
-                step(b)
-            graphs.append(gph)
-    torch.cuda.synchronize()
-    replays = args.steps // npipe
-    nrep = len(graphs)
-
-    with torch.cuda.stream(stream):
-        for k in range((args.warmup + npipe - 1) // npipe):
-            graphs[k % nrep].replay()
-    torch.cuda.synchronize()
-
-    # ---- timed region
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
-        with torch.cuda.stream(stream):
-            ev0.record(stream)
-            for k in range(replays):
-                graphs[k % nrep].replay()
-            ev1.record(stream)
-        torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    if dist:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    # ---- timed region (headline mode)
+    clk = ClockSampler(local_rank)
+    ms, npipe = timed(args.mode, args.steps, args.warmup, clk)
     value = world * args.steps / (ms / 1e3)
-    log(f"timed: {args.steps} steps in {ms:.3f} ms -> {value:.1f} modules/s")
+    log(f"timed ({args.mode}): {args.steps} steps in {ms:.3f} ms -> {value:.1f} modules/s")
+
+    # ---- the other variant (inference module / training step), same protocol
+    variants = {}
+    other = "infer" if args.mode == "train" else "train"
+    if args.variant_steps > 0:
+        vsteps = args.variant_steps - args.variant_steps % max(1, args.pipeline)
+        vms, _ = timed(other, vsteps, args.warmup)
+        variants[other] = {
+            "value": round(world * vsteps / (vms / 1e3), 3), "unit": UNIT,
+            "ms_per_step": round(vms / vsteps, 5), "steps": vsteps,
+            "what": ("row_norm + plain compose_fwd (inference module)" if other == "infer" else
+                     "row_norm + dual compose_fwd + compose_bwd with d_mag (training step)")}
+        log(f"variant {other}: {variants[other]['value']} modules/s")
 
     # ---- per-kernel live durations (event-bracketed launches, same kernels/buffers)
     prof_steps = min(args.steps, args.prof_steps)
@@ -342,7 +389,7 @@ def run_gpu(args, rank, world, local_rank, dist):
     with torch.cuda.stream(stream):
         for k in range(prof_steps):
             torch.cuda._sleep(2_000_000)       # queue the whole step behind a spin so the
-            step(sets[k % nbuf])               # brackets time the device, not the host
+            step(sets[k % nbuf], args.mode)    # brackets time the device, not the host
     rep = dfx.profile_report()
     dfx.profile(False)
     peaks_hbm, peak_tf_burst, peak_tf_sus, peak_src = load_peaks()
@@ -396,15 +443,20 @@ def run_gpu(args, rank, world, local_rank, dist):
     if args.e2e_steps > 0:
         hp = lambda t: t.cpu().pin_memory()
         b0 = sets[0]
-        hW, hA, hB, hm = hp(b0["W"]), hp(b0["A"]), hp(b0["B"]), hp(b0["m"])
-        hbase, hlora = hp(b0["base"]), hp(b0["lora"])
-        hdelta = torch.empty_like(hbase).pin_memory()
+        h = {k: hp(b0[k]) for k in ("W", "A", "B", "m", "base", "lora", "dy")}
+        out = {k: torch.empty_like(h["base"]).pin_memory() for k in ("delta", "dl", "db")}
         hg = torch.empty(d_out, dtype=torch.float32).pin_memory()
+        hdm = torch.empty(d_out, dtype=torch.float32).pin_memory()
         code = {torch.bfloat16: P.BF16, torch.float16: P.F16, torch.float32: P.F32}[tdt]
 
         def e2e_step():
-            dfx.module_fwd_host(code, hW, hA, hB, hm, hbase, hlora, s, d_out, d_in, r, rows, cs,
-                                hdelta, hg)
+            if args.mode == "infer":
+                dfx.module_fwd_host(code, h["W"], h["A"], h["B"], h["m"], h["base"], h["lora"], s,
+                                    d_out, d_in, r, rows, cs, out["delta"], hg)
+            else:
+                dfx.module_train_host(code, h["W"], h["A"], h["B"], h["m"], h["base"], h["lora"],
+                                      h["dy"], s, d_out, d_in, r, rows, cs, out["delta"],
+                                      out["dl"], out["db"], hdm, hg)
 
         e2e_step()  # stage buffers
         if dist:
@@ -417,15 +469,21 @@ def run_gpu(args, rank, world, local_rank, dist):
             t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        # result check on the host copy: the same delta the device path produced
+        # result check on the host copies: the same outputs the device path produced
         torch.cuda.synchronize()
-        assert torch.equal(hdelta.to(dev), b0["delta"]) or args.steps == 0, "e2e delta mismatch"
-        eb = hW.element_size()
+        assert torch.equal(out["delta"].to(dev), b0["delta"]), "e2e delta mismatch"
+        if args.mode == "train":
+            assert torch.equal(out["dl"].to(dev), b0["dl"]), "e2e d_lora mismatch"
+            assert torch.equal(hdm.to(dev), b0["dm"]), "e2e d_mag mismatch"
+        eb = h["W"].element_size()
+        nact = rows * d_out * eb
+        n_in, n_out = (2, 1) if args.mode == "infer" else (3, 3)
         e2e = {"value": round(world * args.e2e_steps / e2e_s, 2), "unit": UNIT,
-               "h2d_bytes_per_step": int((d_out * d_in + r * d_in + d_out * r + 2 * rows * d_out) * eb
+               "h2d_bytes_per_step": int((d_out * d_in + r * d_in + d_out * r) * eb + n_in * nact
                                          + 4 * d_out),
-               "d2h_bytes_per_step": int(rows * d_out * eb + 4 * d_out),
-               "api": "dfx_module_fwd_host (pinned host buffers, H2D+kernels+D2H, blocking)",
+               "d2h_bytes_per_step": int(n_out * nact + 4 * d_out * (1 if args.mode == "infer" else 2)),
+               "api": ("dfx_module_fwd_host" if args.mode == "infer" else "dfx_module_train_host") +
+                      " (pinned host buffers, H2D + kernels + D2H, blocking)",
                "steps": args.e2e_steps}
         log(f"e2e: {e2e['value']} modules/s")
 
@@ -434,7 +492,7 @@ def run_gpu(args, rank, world, local_rank, dist):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cores = host_cores()
-            rate, det = cpu_reference_rate(cfg, cores, rounds=1, warm=0, log=log)
+            rate, det = cpu_reference_rate(cfg, cores, mode=args.mode, rounds=1, warm=0, log=log)
             cpu = {"value": round(rate, 6), "unit": UNIT, "cores": cores, "kind": "reference",
                    "sample": det["sample"], "t_module_1core_s": round(det["t_module_1core_s"], 2)}
         except Exception as e:
@@ -442,25 +500,27 @@ def run_gpu(args, rank, world, local_rank, dist):
 
     clocks = clk.summary()
     if rank == 0:
+        what = ("row_norm + magnitude + dual compose_fwd + compose_bwd (d_lora, d_base, d_mag)"
+                if args.mode == "train" else "row_norm + magnitude + compose_fwd")
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
             "data": "synthetic (seeded torch.randn on device; m = norm*(1+N(0,0.0015)))",
             "config": {"workload": f"{args.config}: single DoRA module d_out={d_out} d_in={d_in} "
-                                   f"r={r} {cfg['dtype']}, tokens={rows}: row_norm + magnitude + "
-                                   f"compose_fwd per step",
-                       "d_out": d_out, "d_in": d_in, "r": r, "tokens": rows,
+                                   f"r={r} {cfg['dtype']}, tokens={rows}: {what} per step",
+                       "mode": args.mode, "d_out": d_out, "d_in": d_in, "r": r, "tokens": rows,
                        "chunk_plan": [cs, nchunks], "s": s,
                        "parallelism": f"module-sharded x{world} (no collective)",
-                       "l2": f"inputs > L2 (W {d_out * d_in * 2 >> 20} MiB + base/lora "
-                             f"{2 * rows * d_out * 2 >> 20} MiB per module), {nbuf} rotating "
-                             f"module buffer sets",
+                       "l2": f"inputs > L2 (W {d_out * d_in * 2 >> 20} MiB + activations "
+                             f"{(3 if args.mode == 'infer' else 7) * rows * d_out * 2 >> 20} MiB per "
+                             f"module), {nbuf} rotating module buffer sets",
                        "timing": "CUDA graphs replayed on one stream, CUDA events, max over ranks",
                        "pipeline": (f"{npipe} modules per graph; module i's compose overlaps "
                                     f"module i+1's norm on a second stream" if npipe > 1
                                     else "serial")},
             "roofline": roofline, "roofline_norm_stage": norm_roof, "kernels": kernels,
+            "variants": variants,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "gpu_launches_per_step": launches_per_step,
@@ -483,7 +543,7 @@ def run_reference(args, rank, world):
     rounds = max(1, min(args.steps, 20))
     warm = min(args.warmup, 1)
     t0 = time.perf_counter()
-    rate, det = cpu_reference_rate(cfg, cores, rounds=rounds, warm=warm, log=log)
+    rate, det = cpu_reference_rate(cfg, cores, mode=args.mode, rounds=rounds, warm=warm, log=log)
     wall = time.perf_counter() - t0
     line = {
         "impl": "reference", "metric": METRIC, "value": round(rate, 6), "unit": UNIT,
@@ -491,8 +551,10 @@ def run_reference(args, rank, world):
         "ms_per_step": round(1e3 / rate, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (numpy, seeded)",
         "config": {"workload": f"{args.config}: reference factored_row_norm + magnitude_scale + "
-                               f"fused_compose (proj/src, CPU, 1 thread per module)",
-                   **{k: cfg[k] for k in ("d_out", "d_in", "r", "tokens")}},
+                               + ("dual_output_compose + compose_backward (mag_grad)"
+                                  if args.mode == "train" else "fused_compose")
+                               + " (proj/src, CPU, 1 thread per module)",
+                   "mode": args.mode, **{k: cfg[k] for k in ("d_out", "d_in", "r", "tokens")}},
         "cpu_baseline": {"value": round(rate, 6), "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": det["sample"]},
         "e2e": {"value": round(rate, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -515,8 +577,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pipeline", type=int, default=8,
                     help="modules per graph, software-pipelined on two streams (1 = serial)")
-    ap.add_argument("--stage", default="module", choices=["module", "norm", "compose"],
-                    help="analysis only: time one half of the module")
+    ap.add_argument("--mode", default="train", choices=["train", "infer"],
+                    help="train: norm + dual compose + backward (headline); infer: norm + compose")
+    ap.add_argument("--variant-steps", type=int, default=400,
+                    help="steps for the other mode's variant line (0 = skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

@@ -145,6 +145,17 @@ int dfx_module_fwd_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void
                         double s, int64_t d_out, int64_t d_in, int64_t r, int64_t rows,
                         int64_t chunk_size, void* delta, float* g);
 
+/* One whole DoRA module TRAINING step from HOST buffers (layer_forward's hot path with a
+ * trainable magnitude, then layer_backward's compose_backward, layer.cpp:61-89,139):
+ * H2D of W, A, B, m, base, lora, dY; row norm + g; dual-output compose (inner stays on
+ * the device); compose backward with the magnitude gradient; D2H of delta, d_lora,
+ * d_base, d_mag and g.  Host buffers should be pinned.  Blocks until done. */
+int dfx_module_train_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A,
+                          const void* B, const float* m, const void* base, const void* lora,
+                          const void* dy, double s, int64_t d_out, int64_t d_in, int64_t r,
+                          int64_t rows, int64_t chunk_size, void* delta, void* d_lora,
+                          void* d_base, float* d_mag, float* g);
+
 /* 1 when dfx_row_norm takes the tcgen05/TMA path for this (dtype, shape). */
 int dfx_norm_uses_tensor_cores(dfx_dtype dtype, int64_t d_out, int64_t d_in, int64_t r);
 

@@ -76,6 +76,8 @@ SIGNATURES = {
                                _vp]),
     "dfx_module_fwd_host": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _f64, _i64, _i64,
                                    _i64, _i64, _i64, _vp, _vp]),
+    "dfx_module_train_host": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f64, _i64,
+                                     _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "dfx_norm_uses_tensor_cores": (_int, [_int, _i64, _i64, _i64]),
 }
 
@@ -227,6 +229,15 @@ class Dfx:
                                                  _ptr(m), _ptr(base), _ptr(lora), float(s),
                                                  d_out, d_in, r, rows, chunk_size, _ptr(delta),
                                                  _ptr(g)))
+
+    def module_train_host(self, dtype, W, A, B, m, base, lora, dy, s, d_out, d_in, r, rows,
+                          chunk_size, delta, d_lora, d_base, d_mag, g):
+        """Training step from host (pinned CPU tensor) buffers; blocking."""
+        self._check(self.lib.dfx_module_train_host(self.ctx, dtype, _ptr(W), _ptr(A), _ptr(B),
+                                                   _ptr(m), _ptr(base), _ptr(lora), _ptr(dy),
+                                                   float(s), d_out, d_in, r, rows, chunk_size,
+                                                   _ptr(delta), _ptr(d_lora), _ptr(d_base),
+                                                   _ptr(d_mag), _ptr(g)))
 
     # ------------------------------------------------------------ profiling
     def profile(self, on: bool = True):

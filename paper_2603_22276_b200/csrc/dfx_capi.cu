@@ -628,4 +628,114 @@ int dfx_module_fwd_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void
     return finish_call(e, "dfx_module_fwd_host");
 }
 
+int dfx_module_train_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A,
+                          const void* B, const float* m, const void* base, const void* lora,
+                          const void* dy, double s, int64_t d_out, int64_t d_in, int64_t r,
+                          int64_t rows, int64_t chunk_size, void* delta, void* d_lora,
+                          void* d_base, float* d_mag, float* g) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    rc = check_norm_args(dtype, W, A, B, d_out, d_in, r, chunk_size);
+    if (rc) return rc;
+    if (rows < 0 || !m || !g || !d_mag ||
+        (rows > 0 && (!base || !lora || !dy || !delta || !d_lora || !d_base)))
+        return fail(DFX_EINVAL, "dfx_module_train_host: null operand");
+    cudaError_t e = cudaSuccess;
+    if (!ctx->st_h2d) {
+        if ((e = cudaStreamCreateWithFlags(&ctx->st_h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&ctx->st_comp, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&ctx->st_d2h, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e, "stream create");
+    }
+    const size_t eb = dtype == DFX_F32 ? 4 : 2;
+    const size_t nW = size_t(d_out) * d_in, nA = size_t(r) * d_in, nB = size_t(d_out) * r;
+    const size_t nact = size_t(rows) * d_out;
+    const size_t sizes[14] = {nW * eb, nA * eb, nB * eb, size_t(d_out) * 4, size_t(d_out) * 4,
+                              size_t(d_out) * 4, nact * eb, nact * eb, nact * eb, nact * eb,
+                              nact * eb, nact * eb, nact * eb, size_t(d_out) * 4};
+    void* buf[14];
+    for (int i = 0; i < 14; ++i) {
+        buf[i] = stage_buf(ctx, i, sizes[i], &e);
+        if (e) return cuda_fail(e, "stage alloc");
+    }
+    void *dW = buf[0], *dA = buf[1], *dB = buf[2];
+    float *dm = static_cast<float*>(buf[3]), *dg = static_cast<float*>(buf[4]);
+    float* dwn = static_cast<float*>(buf[5]);
+    void *dbase = buf[6], *dlora = buf[7], *ddelta = buf[8], *dinner = buf[9], *ddy = buf[10];
+    void *ddl = buf[11], *ddb = buf[12];
+    float* ddm = static_cast<float*>(buf[13]);
+
+    std::vector<cudaEvent_t> evs;
+    auto event = [&]() {
+        cudaEvent_t ev;
+        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        evs.push_back(ev);
+        return ev;
+    };
+    // weights first: the norm overlaps the activation upload
+    cudaMemcpyAsync(dA, A, nA * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
+    cudaMemcpyAsync(dB, B, nB * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
+    cudaMemcpyAsync(dm, m, d_out * 4, cudaMemcpyHostToDevice, ctx->st_h2d);
+    cudaMemcpyAsync(dW, W, nW * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
+    cudaEvent_t ev_w = event();
+    cudaEventRecord(ev_w, ctx->st_h2d);
+    cudaStreamWaitEvent(ctx->st_comp, ev_w, 0);
+    rc = run_norm(ctx, dtype, dW, dA, dB, d_out, d_in, r, s, chunk_size, nullptr, nullptr,
+                  nullptr, dm, dtype, dwn, dg, dtype, ctx->st_comp, "dfx_module_train_host/norm");
+    if (rc) return rc;
+    cudaEvent_t ev_norm = event();
+    cudaEventRecord(ev_norm, ctx->st_comp);
+    cudaStreamWaitEvent(ctx->st_d2h, ev_norm, 0);
+    cudaMemcpyAsync(g, dg, d_out * 4, cudaMemcpyDeviceToHost, ctx->st_d2h);
+
+    // forward in row chunks (upload c+1 while composing c and downloading c-1); the dual
+    // output's inner stays on the device for the magnitude gradient
+    const int64_t nchunk = rows >= 1024 ? 8 : 1;
+    const int64_t crow = rows > 0 ? (rows + nchunk - 1) / nchunk : 1;
+    for (int64_t r0 = 0; r0 < rows; r0 += crow) {
+        const int64_t nr = std::min(crow, rows - r0);
+        const size_t off = size_t(r0) * d_out * eb, bytes = size_t(nr) * d_out * eb;
+        cudaMemcpyAsync(static_cast<char*>(dbase) + off, static_cast<const char*>(base) + off,
+                        bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        cudaMemcpyAsync(static_cast<char*>(dlora) + off, static_cast<const char*>(lora) + off,
+                        bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        cudaEvent_t ein = event();
+        cudaEventRecord(ein, ctx->st_h2d);
+        cudaStreamWaitEvent(ctx->st_comp, ein, 0);
+        int launches = 0;
+        e = dfx::launch_compose_fwd(dtype, static_cast<char*>(dbase) + off,
+                                    static_cast<char*>(dlora) + off, dg, static_cast<float>(s), nr,
+                                    d_out, static_cast<char*>(ddelta) + off,
+                                    static_cast<char*>(dinner) + off, ctx->st_comp, &launches);
+        ctx->launches += launches;
+        if (e != cudaSuccess) return cuda_fail(e, "dfx_module_train_host/compose");
+        cudaEvent_t eout = event();
+        cudaEventRecord(eout, ctx->st_comp);
+        cudaStreamWaitEvent(ctx->st_d2h, eout, 0);
+        cudaMemcpyAsync(static_cast<char*>(delta) + off, static_cast<char*>(ddelta) + off, bytes,
+                        cudaMemcpyDeviceToHost, ctx->st_d2h);
+    }
+    // backward: dY streams up behind the forward's activations; the serial d_mag chain
+    // needs every row, so the backward runs once dY is resident
+    cudaMemcpyAsync(ddy, dy, nact * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
+    cudaEvent_t ev_dy = event();
+    cudaEventRecord(ev_dy, ctx->st_h2d);
+    cudaStreamWaitEvent(ctx->st_comp, ev_dy, 0);
+    int launches = 0;
+    e = dfx::launch_compose_bwd(dtype, ddy, dg, static_cast<float>(s), dinner, dwn, rows, d_out,
+                                ddl, ddb, ddm, ctx->st_comp, &launches);
+    ctx->launches += launches;
+    if (e != cudaSuccess) return cuda_fail(e, "dfx_module_train_host/backward");
+    cudaEvent_t ev_bwd = event();
+    cudaEventRecord(ev_bwd, ctx->st_comp);
+    cudaStreamWaitEvent(ctx->st_d2h, ev_bwd, 0);
+    cudaMemcpyAsync(d_lora, ddl, nact * eb, cudaMemcpyDeviceToHost, ctx->st_d2h);
+    cudaMemcpyAsync(d_base, ddb, nact * eb, cudaMemcpyDeviceToHost, ctx->st_d2h);
+    cudaMemcpyAsync(d_mag, ddm, d_out * 4, cudaMemcpyDeviceToHost, ctx->st_d2h);
+    e = cudaStreamSynchronize(ctx->st_d2h);
+    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return finish_call(e, "dfx_module_train_host");
+}
+
 }  // extern "C"

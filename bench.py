@@ -383,6 +383,48 @@ def run_gpu(args, rank, world, local_rank, dist):
                      "row_norm + dual compose_fwd + compose_bwd with d_mag (training step)")}
         log(f"variant {other}: {variants[other]['value']} modules/s")
 
+    # ---- LoRA-up GEMM fused with compose + residual (layer forward
+    # epilogue, training outputs y and inner) vs the unfused sequence (cuBLAS lora GEMM,
+    # dual compose, residual add)
+    if args.lora_steps > 0 and cfg["dtype"] != "fp32":
+        b = sets[0]
+        mid = torch.randn(rows, r, device=dev, generator=gen).to(tdt)
+        y = torch.empty_like(b["base"])
+
+        def batch_time(fn, n):
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    fn()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(n):
+                    fn()
+                e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) * 1e3 / n
+
+        fused = lambda: dfx.lora_compose(mid, b["B"], b["base"], b["g"], s, y=y, inner=b["inner"])
+
+        def unfused():
+            torch.matmul(mid, b["B"].T, out=b["lora"])
+            dfx.compose_fwd(b["base"], b["lora"], b["g"], s, b["delta"], b["inner"])
+            torch.add(b["base"], b["delta"], out=y)
+
+        tf, tu = batch_time(fused, args.lora_steps), batch_time(unfused, args.lora_steps)
+        eb = 2
+        byts = 3 * rows * d_out * eb + (rows * r + d_out * r) * eb + 4 * d_out
+        peaks_hbm_l = load_peaks()[0]
+        variants["layer_fwd_lora_compose"] = {
+            "what": "y, inner = residual/compose(base, round(mid . B^T)) for tokens x d_out, "
+                    "K = r (layer.cpp:57-120)",
+            "fused_us": round(tf, 2), "unfused_us": round(tu, 2), "speedup": round(tu / tf, 3),
+            "fused_hbm_gbs": round(byts / (tf * 1e-6) / 1e9, 1),
+            "fused_hbm_frac": round(byts / (tf * 1e-6) / 1e9 / peaks_hbm_l, 4),
+            "algorithmic_bytes": byts,
+            "unfused": "cuBLAS bf16 GEMM -> lora (HBM), dfx_compose_fwd dual, torch.add residual"}
+        log(f"lora_compose fused {tf:.1f} us vs unfused {tu:.1f} us")
+
     # ---- per-kernel live durations (event-bracketed launches, same kernels/buffers)
     prof_steps = min(args.steps, args.prof_steps)
     dfx.profile(True)
@@ -579,6 +621,8 @@ def main():
                     help="modules per graph, software-pipelined on two streams (1 = serial)")
     ap.add_argument("--mode", default="train", choices=["train", "infer"],
                     help="train: norm + dual compose + backward (headline); infer: norm + compose")
+    ap.add_argument("--lora-steps", type=int, default=50,
+                    help="calls timed for the fused LoRA-GEMM + compose variant (0 = skip)")
     ap.add_argument("--variant-steps", type=int, default=400,
                     help="steps for the other mode's variant line (0 = skip)")
     args = ap.parse_args()

@@ -136,6 +136,19 @@ int dfx_compose_bwd(dfx_ctx* ctx, dfx_dtype dtype, const void* dy, const float* 
                     const void* inner, const float* w_norm, int64_t rows, int64_t d_out,
                     void* d_lora, void* d_base, float* d_mag, dfx_stream_t stream);
 
+/* layer_forward's LoRA-up GEMM fused with the compose and the residual (layer.cpp:57-58,
+ * 73-120): lora = round(mid . B^T) is formed on the tensor cores and
+ * never reaches HBM; per element delta = round((g-1)*base + g*(s*lora)) (compose.cpp:19-24),
+ * inner = round(s*lora + base), y = round(base + delta) then round(y + bias) when bias != NULL.
+ * mid [rows, r], B [d_out, r], base / outputs [rows, d_out] row-major (bf16 or fp16);
+ * g, bias fp32 [d_out] holding working-dtype values.  Outputs y, delta, inner, lora are each
+ * optional (NULL = not written), at most three per call.  Given the same lora, every output
+ * is bitwise the reference's; lora is an fp32-accumulated tensor-core GEMM. */
+int dfx_lora_compose(dfx_ctx* ctx, dfx_dtype dtype, const void* mid, const void* B,
+                     const void* base, const float* g, double s, const float* bias, int64_t rows,
+                     int64_t d_out, int64_t r, void* y, void* delta, void* inner, void* lora,
+                     dfx_stream_t stream);
+
 /* One whole DoRA module forward from HOST buffers (the end-to-end call a host
  * framework makes): H2D of W, A, B, m, base, lora; row norm + g; compose; D2H of
  * delta and g.  Host buffers should be pinned for full PCIe bandwidth.  Blocks

@@ -190,6 +190,33 @@ void orc_compose_fwd(int dtype, const float* base, const float* lora, const floa
     }
 }
 
+/* working_matmul (layer.cpp:15-17 over matrix.cpp:53-78): C = A . B^T with A [m, k] and
+ * Bt [n, k] row-major, fp32 accumulation ascending in k, result rounded to dtype. */
+void orc_working_matmul_nt(int dtype, const float* a, const float* bt, size_t m, size_t n,
+                           size_t k, float* out) {
+    for (size_t i = 0; i < m; ++i) {
+        for (size_t j = 0; j < n; ++j) {
+            float acc = 0.0f;
+            for (size_t kk = 0; kk < k; ++kk) acc += a[i * k + kk] * bt[j * k + kk];
+            out[i * n + j] = rnd_f(acc, dtype);
+        }
+    }
+}
+
+/* Residual and bias after the compose (layer.cpp:108-120): y = round(base + delta), then
+ * y = round(y + bias[j]) when bias is given; all adds in fp32. */
+void orc_residual(int dtype, const float* base, const float* delta, const float* bias,
+                  size_t rows, size_t d_out, float* y) {
+    for (size_t i = 0; i < rows; ++i) {
+        for (size_t j = 0; j < d_out; ++j) {
+            const size_t e = i * d_out + j;
+            float v = rnd_f(base[e] + delta[e], dtype);
+            if (bias) v = rnd_f(v + bias[j], dtype);
+            y[e] = v;
+        }
+    }
+}
+
 /* naive_compose (compose.cpp:47-68): every intermediate re-rounded to dtype. */
 void orc_naive_compose(int dtype, const float* base, const float* lora, const float* g, double s,
                        size_t rows, size_t d_out, float* delta) {

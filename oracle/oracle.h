@@ -60,6 +60,10 @@ void orc_compose_fwd(int dtype, const float* base, const float* lora, const floa
                      size_t rows, size_t d_out, float* delta, float* inner);
 
 /* naive_compose (compose.cpp:47-68) — the stability lab's counterexample. */
+void orc_working_matmul_nt(int dtype, const float* a, const float* bt, size_t m, size_t n,
+                           size_t k, float* out);
+void orc_residual(int dtype, const float* base, const float* delta, const float* bias,
+                  size_t rows, size_t d_out, float* y);
 void orc_naive_compose(int dtype, const float* base, const float* lora, const float* g, double s,
                        size_t rows, size_t d_out, float* delta);
 

@@ -65,6 +65,8 @@ class Oracle:
         L.orc_magnitude_scale.argtypes = [C.c_int, _dp, _fp, _sz, _fp]
         L.orc_compose_fwd.argtypes = [C.c_int, _fp, _fp, _fp, C.c_double, _sz, _sz, _fp, _fp]
         L.orc_naive_compose.argtypes = [C.c_int, _fp, _fp, _fp, C.c_double, _sz, _sz, _fp]
+        L.orc_working_matmul_nt.argtypes = [C.c_int, _fp, _fp, _sz, _sz, _sz, _fp]
+        L.orc_residual.argtypes = [C.c_int, _fp, _fp, _fp, _sz, _sz, _fp]
         L.orc_compose_bwd.argtypes = [C.c_int, _fp, _fp, C.c_double, _fp, _fp, _sz, _sz, C.c_int,
                                       _fp, _fp, _fp]
         L.orc_dense_row_norm_f64.argtypes = [_fp, _fp, _fp, _sz, _sz, _sz, C.c_double, _dp]
@@ -123,6 +125,20 @@ class Oracle:
         inner = np.zeros_like(base) if need_inner else None
         self.L.orc_compose_fwd(dtype, _f(base), _f(lora), _f(g), s, rows, d_out, _f(delta), _f(inner))
         return delta, inner
+
+    def working_matmul_nt(self, dtype, a, bt):
+        """round_dtype(a @ bt.T) with the reference's serial-k fp32 accumulation."""
+        m, k = a.shape
+        n = bt.shape[0]
+        out = np.zeros((m, n), np.float32)
+        self.L.orc_working_matmul_nt(dtype, _f(a), _f(bt), m, n, k, _f(out))
+        return out
+
+    def residual(self, dtype, base, delta, bias=None):
+        rows, d_out = base.shape
+        y = np.zeros_like(base)
+        self.L.orc_residual(dtype, _f(base), _f(delta), _f(bias), rows, d_out, _f(y))
+        return y
 
     def naive_compose(self, dtype, base, lora, g, s):
         rows, d_out = base.shape
@@ -185,6 +201,8 @@ class Reference:
         L.ref_compose.argtypes = [C.c_int, C.c_int, _fp, _fp, _dp, C.c_double, _sz, _sz, _fp, _fp]
         L.ref_compose_bwd.argtypes = [C.c_int, _fp, _dp, C.c_double, _fp, _dp, _sz, _sz, C.c_int,
                                       _fp, _fp, _dp]
+        L.ref_layer_forward.argtypes = [C.c_int, _fp, _fp, _fp, _fp, C.c_double, _dp, _dp, _sz, _sz,
+                                        _sz, _sz, _fp, _fp, _fp, _fp, _fp, _dp, _dp]
         L.ref_dense_row_norm_f64.argtypes = [_fp, _fp, _fp, _sz, _sz, _sz, C.c_double, _dp]
         L.ref_seeded_gaussian.argtypes = [_sz, _sz, C.c_uint64, C.c_int, _fp]
         L.ref_gaussian_fixture.argtypes = [_sz, _sz, C.c_double, C.c_double, C.c_uint64, C.c_int, _fp]
@@ -258,6 +276,24 @@ class Reference:
                                   int(mag_grad), _f(d_lora), _f(d_base), _d(d_mag)) != 0:
             raise ValueError("compose_backward threw")
         return d_lora, d_base, d_mag
+
+    def layer_forward(self, dtype, x, w, a, b, s, m, bias=None):
+        """The reference's layer_forward; returns dict of y, lora_mid, base_out, lora_out,
+        inner, g, w_norm."""
+        rows, d_in = x.shape
+        d_out, r = b.shape
+        o = {k: np.zeros((rows, d_out), np.float32) for k in ("y", "base_out", "lora_out", "inner")}
+        o["lora_mid"] = np.zeros((rows, r), np.float32)
+        o["g"] = np.zeros(d_out, np.float64)
+        o["w_norm"] = np.zeros(d_out, np.float64)
+        m = np.ascontiguousarray(m, np.float64)
+        bias = None if bias is None else np.ascontiguousarray(bias, np.float64)
+        if self.L.ref_layer_forward(dtype, _f(x), _f(w), _f(a), _f(b), s, _d(m), _d(bias), rows,
+                                    d_in, d_out, r, _f(o["y"]), _f(o["lora_mid"]), _f(o["base_out"]),
+                                    _f(o["lora_out"]), _f(o["inner"]), _d(o["g"]),
+                                    _d(o["w_norm"])) != 0:
+            raise ValueError("layer_forward threw")
+        return o
 
     def dense_row_norm_f64(self, w, a, b, s):
         d_out, d_in = w.shape

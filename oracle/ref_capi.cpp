@@ -16,6 +16,7 @@
 
 #include "dorafactor/compose.hpp"
 #include "dorafactor/factored_norm.hpp"
+#include "dorafactor/layer.hpp"
 #include "dorafactor/reference.hpp"
 
 namespace R = dorafactor;  // renamed to dorafactor_ref by the -D flag
@@ -229,6 +230,39 @@ void ref_gaussian_vector(std::size_t n, double mean, double stddev, std::uint64_
 
 std::uint64_t ref_derive_seed(std::uint64_t base, std::uint64_t index) {
     return R::derive_seed(base, index);
+}
+
+// layer_forward (layer.cpp:51-127) on packed inputs: X [rows, d_in], W [d_out, d_in],
+// A [r, d_in], B [d_out, r]; m / bias (nullable) [d_out].  Writes y, lora_mid, base_out,
+// lora_out, inner (when the magnitude trains), g and w_norm.
+int ref_layer_forward(int dtype, const float* x, const float* w, const float* a, const float* b,
+                      double s, const double* m, const double* bias, std::size_t rows,
+                      std::size_t d_in, std::size_t d_out, std::size_t r, float* y, float* lora_mid,
+                      float* base_out, float* lora_out, float* inner, double* g, double* w_norm) {
+    try {
+        R::AdapterPair ad{pack(a, r, d_in, dtype), pack(b, d_out, r, dtype), s};
+        R::Magnitude mag{std::vector<double>(m, m + d_out), spec(dtype)};
+        std::optional<std::vector<double>> bv;
+        if (bias) bv = std::vector<double>(bias, bias + d_out);
+        const R::DoraLinearState st =
+            R::make_layer_state(pack(w, d_out, d_in, dtype), ad, mag, bv, spec(dtype));
+        const R::RealMatrix X = pack(x, rows, d_in, dtype);
+        R::LayerForwardResult res{R::RealMatrix(), {}};
+        {
+            CallTimer t;
+            res = R::layer_forward(st, X);
+        }
+        unpack(res.y, y);
+        if (lora_mid) unpack(res.saved.lora_mid, lora_mid);
+        if (base_out) unpack(res.saved.base_out, base_out);
+        if (lora_out) unpack(res.saved.lora_out, lora_out);
+        if (inner && res.saved.inner) unpack(*res.saved.inner, inner);
+        if (g) std::memcpy(g, res.saved.g.data(), d_out * sizeof(double));
+        if (w_norm) std::memcpy(w_norm, res.saved.w_norm.data(), d_out * sizeof(double));
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
 }
 
 }  // extern "C"

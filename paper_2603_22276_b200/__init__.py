@@ -76,6 +76,8 @@ SIGNATURES = {
                                _vp]),
     "dfx_module_fwd_host": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _f64, _i64, _i64,
                                    _i64, _i64, _i64, _vp, _vp]),
+    "dfx_lora_compose": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _f64, _vp, _i64, _i64, _i64, _vp,
+                                _vp, _vp, _vp, _vp]),
     "dfx_module_train_host": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f64, _i64,
                                      _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "dfx_norm_uses_tensor_cores": (_int, [_int, _i64, _i64, _i64]),
@@ -221,6 +223,16 @@ class Dfx:
         self._check(self.lib.dfx_compose_bwd(self.ctx, dt, _ptr(dy), _ptr(g), float(s),
                                              _ptr(inner), _ptr(w_norm), rows, d_out, _ptr(d_lora),
                                              _ptr(d_base), _ptr(d_mag), _stream(stream)))
+
+    def lora_compose(self, mid, B, base, g, s, y=None, delta=None, inner=None, lora=None,
+                     bias=None, stream=None):
+        """Fused LoRA-up GEMM + compose + residual (device tensors)."""
+        rows, r = mid.shape
+        d_out = B.shape[0]
+        self._check(self.lib.dfx_lora_compose(self.ctx, _dtype_code(mid), _ptr(mid), _ptr(B),
+                                              _ptr(base), _ptr(g), float(s), _ptr(bias), rows,
+                                              d_out, r, _ptr(y), _ptr(delta), _ptr(inner),
+                                              _ptr(lora), _stream(stream)))
 
     def module_fwd_host(self, dtype, W, A, B, m, base, lora, s, d_out, d_in, r, rows,
                         chunk_size, delta, g):

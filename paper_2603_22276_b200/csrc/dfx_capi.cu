@@ -108,6 +108,13 @@ EncodeFn encode_fn() {
 cudaError_t make_tmap_2d(CUtensorMap* out, int dt, const void* base, uint64_t rows, uint64_t cols,
                          uint64_t row_pitch_bytes, uint32_t box_cols, uint32_t box_rows,
                          bool swizzle128) {
+    return make_tmap_2d_sw(out, dt, base, rows, cols, row_pitch_bytes, box_cols, box_rows,
+                           swizzle128 ? 128 : 0);
+}
+
+cudaError_t make_tmap_2d_sw(CUtensorMap* out, int dt, const void* base, uint64_t rows,
+                            uint64_t cols, uint64_t row_pitch_bytes, uint32_t box_cols,
+                            uint32_t box_rows, int swizzle_bytes) {
     EncodeFn fn = encode_fn();
     if (!fn) return cudaErrorNotSupported;
     const CUtensorMapDataType t = dt == kF32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
@@ -119,7 +126,10 @@ cudaError_t make_tmap_2d(CUtensorMap* out, int dt, const void* base, uint64_t ro
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = fn(out, t, 2, const_cast<void*>(base), dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                          swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                          : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                : CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -532,6 +542,31 @@ static void* stage_buf(dfx_ctx* ctx, int slot, size_t bytes, cudaError_t* e) {
     if (*e != cudaSuccess) return nullptr;
     ctx->stage_cap[slot] = bytes;
     return ctx->stage[slot];
+}
+
+int dfx_lora_compose(dfx_ctx* ctx, dfx_dtype dtype, const void* mid, const void* B,
+                     const void* base, const float* g, double s, const float* bias, int64_t rows,
+                     int64_t d_out, int64_t r, void* y, void* delta, void* inner, void* lora,
+                     dfx_stream_t stream) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (dtype != DFX_BF16 && dtype != DFX_F16)
+        return fail(DFX_EUNSUPPORTED, "lora_compose: bf16 / fp16 only (tcgen05 kind::f16)");
+    if (rows < 0 || d_out < 0 || r <= 0) return fail(DFX_EINVAL, "lora_compose: shape");
+    if (d_out % 8 != 0 || r % 8 != 0)
+        return fail(DFX_EINVAL, "lora_compose: d_out and r must be multiples of 8 (16-byte rows)");
+    const int n_out = (y != nullptr) + (delta != nullptr) + (inner != nullptr) + (lora != nullptr);
+    if (n_out > 3) return fail(DFX_EINVAL, "lora_compose: at most three outputs per call");
+    if (rows > 0 && d_out > 0 && (!mid || !B || !base || !g || n_out == 0))
+        return fail(DFX_EINVAL, "lora_compose: null operand");
+    if ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(bias)) & 15u)
+        return fail(DFX_EINVAL, "lora_compose: g and bias must be 16-byte aligned");
+    int launches = 0;
+    const cudaError_t e = dfx::launch_lora_compose(dtype, mid, B, base, g, static_cast<float>(s),
+                                                   bias, rows, d_out, r, y, delta, inner, lora,
+                                                   stream, &launches);
+    ctx->launches += launches;
+    return finish_call(e, "dfx_lora_compose");
 }
 
 int dfx_module_fwd_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A,

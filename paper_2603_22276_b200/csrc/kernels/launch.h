@@ -18,6 +18,10 @@ inline int elem_bytes(int dt) { return dt == kF32 ? 4 : 2; }
 cudaError_t make_tmap_2d(CUtensorMap* out, int dt, const void* base, uint64_t rows, uint64_t cols,
                          uint64_t row_pitch_bytes, uint32_t box_cols, uint32_t box_rows,
                          bool swizzle128);
+// Same with an explicit swizzle span in bytes (0, 32, 64 or 128).
+cudaError_t make_tmap_2d_sw(CUtensorMap* out, int dt, const void* base, uint64_t rows,
+                            uint64_t cols, uint64_t row_pitch_bytes, uint32_t box_cols,
+                            uint32_t box_rows, int swizzle_bytes);
 
 // ---------------------------------------------------------------- compose
 cudaError_t launch_compose_fwd(int dt, const void* base, const void* lora, const float* g, float sf,
@@ -27,6 +31,13 @@ cudaError_t launch_compose_fwd(int dt, const void* base, const void* lora, const
 cudaError_t launch_compose_bwd(int dt, const void* dy, const float* g, float sf, const void* inner,
                                const float* w_norm, int64_t rows, int64_t d_out, void* d_lora,
                                void* d_base, float* d_mag, cudaStream_t st, int* launches);
+
+// LoRA-up GEMM (mid . B^T on tcgen05) fused with compose + residual (lora_compose.cu).
+// Outputs y / delta / inner / lora are each optional (at most three at once).
+cudaError_t launch_lora_compose(int dt, const void* mid, const void* b, const void* base,
+                                const float* g, float s, const float* bias, int64_t rows,
+                                int64_t d_out, int64_t r, void* y, void* delta, void* inner,
+                                void* lora, cudaStream_t st, int* launches);
 
 // ------------------------------------------------------------------- norm
 struct NormArgs {

@@ -31,7 +31,8 @@ def main():
     for i in range(nb):
         d = dict(W=torch.randn(d_out, d_in, device="cuda").to(bf), A=torch.randn(r, d_in, device="cuda").to(bf),
                  B=torch.randn(d_out, r, device="cuda").to(bf), base=torch.randn(rows, d_out, device="cuda").to(bf),
-                 lora=torch.randn(rows, d_out, device="cuda").to(bf))
+                 lora=torch.randn(rows, d_out, device="cuda").to(bf),
+                 mid=torch.randn(rows, r, device="cuda").to(bf))
         d.update(wn=torch.empty(d_out, device="cuda"), g=torch.ones(d_out, device="cuda") * 1.001,
                  m=torch.ones(d_out, device="cuda") * 90.0, delta=torch.empty_like(d["base"]),
                  inner=torch.empty_like(d["base"]), dl=torch.empty_like(d["base"]),
@@ -45,6 +46,9 @@ def main():
         "bwd": lambda d: dfx.compose_bwd(d["base"], d["g"], s, d["dl"], d["db"], inner=d["lora"],
                                          w_norm=d["wn"], d_mag=d["dm"]),
     }
+    ops["lora_fused"] = lambda d: dfx.lora_compose(d["mid"], d["B"], d["base"], d["g"], s,
+                                                   y=d["dl"], inner=d["inner"])
+    ops["lora_gemm_cublas"] = lambda d: torch.matmul(d["mid"], d["B"].T, out=d["lora"])
     out = []
     for w in a.what.split(","):
         f = ops[w]

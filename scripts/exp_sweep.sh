@@ -1,5 +1,2 @@
 #!/bin/bash
-O=gpurun_out/exp.txt; : > $O
-E="timeout 60 python scripts/exp_kernels.py"
-for sv in 8 7 6 4 2; do DFX_BWD_SV=$sv $E --what bwd --tag sv$sv >> $O 2>&1; done
-for sv in 8 7 4; do DFX_BWD_SV=$sv $E --config c1 --what bwd --tag sv$sv >> $O 2>&1; done
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:lora_compose -s 2 -c 1 -o gpurun_out/ncu_lora4 python scripts/exp_kernels.py --what lora_fused --iters 1 > gpurun_out/ncu_lora.log 2>&1

@@ -170,3 +170,31 @@ def test_reference_criterion1_reaches_1_44e_5(oracle):
                     want = o.dense_row_norm_f64(W, A, B, s)
                     worst = max(worst, np.max(np.abs(got - want) / np.maximum(want, 1e-30)))
     assert 1.3e-5 < worst < 1.6e-5
+
+
+def test_layer_forward_pinned(oracle, reference):
+    """oracle.c's working_matmul_nt + compose + residual restate the reference's
+    layer_forward (layer.cpp:51-127) bitwise: mid, lora, base, inner and y (with bias)."""
+    o, R = oracle, reference
+    for dt in (0, 1, 2):
+        seed = o.derive_seed(31337, dt)
+        rows, d_in, d_out, r = 24, 80, 40, 8
+        x = o.gaussian_fixture(rows, d_in, 0.0, 1.0, o.derive_seed(seed, 1), dt)
+        w = o.gaussian_fixture(d_out, d_in, 0.0, 0.1, o.derive_seed(seed, 2), dt)
+        a = o.gaussian_fixture(r, d_in, 0.0, 0.1, o.derive_seed(seed, 3), dt)
+        b = o.gaussian_fixture(d_out, r, 0.0, 0.1, o.derive_seed(seed, 4), dt)
+        m = np.abs(o.gaussian_vector(d_out, 1.0, 0.2, o.derive_seed(seed, 5)))
+        bias = np.array([o.round_to_dtype(v, dt)
+                         for v in o.gaussian_vector(d_out, 0.0, 0.3, o.derive_seed(seed, 6))])
+        s = 0.7
+        ref = R.layer_forward(dt, x, w, a, b, s, m, bias)
+        mid = o.working_matmul_nt(dt, x, a)
+        lora = o.working_matmul_nt(dt, mid, b)
+        base = o.working_matmul_nt(dt, x, w)
+        assert np.array_equal(mid, ref["lora_mid"])
+        assert np.array_equal(lora, ref["lora_out"])
+        assert np.array_equal(base, ref["base_out"])
+        g = ref["g"].astype(np.float32)
+        delta, inner = o.compose_fwd(dt, base, lora, g, s, need_inner=True)
+        assert np.array_equal(inner, ref["inner"])
+        assert np.array_equal(o.residual(dt, base, delta, bias.astype(np.float32)), ref["y"])

@@ -89,6 +89,13 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
     return r;
 }
 
+__device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                       uint32_t d) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+                 "r"(d)
+                 : "memory");
+}
+
 template <typename T> struct LcT;
 template <> struct LcT<__nv_bfloat16> {
     static __device__ __forceinline__ float rnd(float x) {
@@ -253,7 +260,8 @@ __global__ void __launch_bounds__(kLThreads, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tmem_empty[slot]);
                 }
-                uint8_t* orow = obase + (nslice & 1) * p.n_out * kSlice + row * (kLSlice * 2);
+                const uint32_t orow = smem_u32(obase + (nslice & 1) * p.n_out * kSlice) +
+                                      static_cast<uint32_t>(row * (kLSlice * 2));
                 float4 gq[8], bq[8];                         // the slice's 32 g / bias values
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
@@ -293,8 +301,8 @@ __global__ void __launch_bounds__(kLThreads, 1)
 #pragma unroll
                     for (int kind = 0; kind < kMaxOut; ++kind) {
                         if (p.slot[kind] < 0) continue;      // output not requested (uniform)
-                        *reinterpret_cast<uint4*>(orow + p.slot[kind] * kSlice + ((k ^ sw) << 4)) =
-                            make_uint4(o[kind][0], o[kind][1], o[kind][2], o[kind][3]);
+                        sts_v4(orow + static_cast<uint32_t>(p.slot[kind] * kSlice + ((k ^ sw) << 4)),
+                               o[kind][0], o[kind][1], o[kind][2], o[kind][3]);
                     }
                 }
                 // hand the slice to the TMA store; the issuer then waits until the store of

@@ -65,6 +65,12 @@ void dfx_ctx_destroy(dfx_ctx* ctx);
 /* Number of kernels launched by this context since creation (evidence counter). */
 int64_t dfx_ctx_launches(const dfx_ctx* ctx);
 
+/* Cap the SMs the row-norm GEMMs plan for (0 = all).  A caller that streams compose kernels
+ * concurrently with the next module's norm (a pipelined layer stack) leaves the remaining SMs
+ * to them; the planner then prefers the 2-SM W.A^T tiling that ingests W once (full r per CTA
+ * pair), which needs fewer SMs.  Results are identical for every budget. */
+int dfx_ctx_set_sm_budget(dfx_ctx* ctx, int sms);
+
 /* Per-kernel device timing.  While enabled, every kernel the context launches is
  * bracketed by CUDA events on its stream.  dfx_profile_report synchronises the device,
  * writes one line per kernel ("name launches total_ms min_ms max_ms\n") into buf and

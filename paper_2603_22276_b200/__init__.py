@@ -76,6 +76,7 @@ SIGNATURES = {
                                _vp]),
     "dfx_module_fwd_host": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _f64, _i64, _i64,
                                    _i64, _i64, _i64, _vp, _vp]),
+    "dfx_ctx_set_sm_budget": (_int, [_vp, _int]),
     "dfx_lora_compose": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _f64, _vp, _i64, _i64, _i64, _vp,
                                 _vp, _vp, _vp, _vp]),
     "dfx_module_train_host": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f64, _i64,
@@ -223,6 +224,10 @@ class Dfx:
         self._check(self.lib.dfx_compose_bwd(self.ctx, dt, _ptr(dy), _ptr(g), float(s),
                                              _ptr(inner), _ptr(w_norm), rows, d_out, _ptr(d_lora),
                                              _ptr(d_base), _ptr(d_mag), _stream(stream)))
+
+    def set_sm_budget(self, sms: int):
+        """Cap the SMs the norm GEMMs plan for (0 = all); see dfx_ctx_set_sm_budget."""
+        self._check(self.lib.dfx_ctx_set_sm_budget(self.ctx, int(sms)))
 
     def lora_compose(self, mid, B, base, g, s, y=None, delta=None, inner=None, lora=None,
                      bias=None, stream=None):

@@ -25,6 +25,7 @@ namespace dfx {
 struct Workspace {
     int device = 0;
     int sms = 0;
+    int sm_budget = 0;      // dfx_ctx_set_sm_budget: cap on the SMs the norm's GEMMs plan for
     std::vector<void*> ptr;
     std::vector<size_t> cap;
     cudaStream_t side = nullptr;
@@ -55,7 +56,8 @@ cudaEvent_t ws_event(Workspace* ws, int idx, cudaError_t* err) {
 
 int ws_sm_count(Workspace* ws) {
     if (!ws->sms) cudaDeviceGetAttribute(&ws->sms, cudaDevAttrMultiProcessorCount, ws->device);
-    return ws->sms > 0 ? ws->sms : 148;
+    const int n = ws->sms > 0 ? ws->sms : 148;
+    return ws->sm_budget > 0 ? std::min(n, std::max(ws->sm_budget, 4)) : n;
 }
 
 void* ws_get(Workspace* ws, int slot, size_t bytes, cudaError_t* err) {
@@ -542,6 +544,13 @@ static void* stage_buf(dfx_ctx* ctx, int slot, size_t bytes, cudaError_t* e) {
     if (*e != cudaSuccess) return nullptr;
     ctx->stage_cap[slot] = bytes;
     return ctx->stage[slot];
+}
+
+int dfx_ctx_set_sm_budget(dfx_ctx* ctx, int sms) {
+    if (!ctx) return fail(DFX_EINVAL, "dfx_ctx_set_sm_budget: null context");
+    if (sms < 0) return fail(DFX_EINVAL, "dfx_ctx_set_sm_budget: negative budget");
+    ctx->ws.sm_budget = sms;
+    return DFX_OK;
 }
 
 int dfx_lora_compose(dfx_ctx* ctx, dfx_dtype dtype, const void* mid, const void* B,

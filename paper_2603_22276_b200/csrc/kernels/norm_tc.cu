@@ -59,6 +59,7 @@ struct TcParams {
     int gram_nt;            // tiles per side
     int tiles;              // tiles per K split (the persistent loop's extent)
     int w_prefetch;         // K blocks of X (W) prefetched into L2 ahead of the loads
+    int nh;                 // pair kernel: UMMAs per K step (N per CTA pair = nh * bn)
 };
 
 __device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
@@ -394,8 +395,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    const int half_n = p.bn / 2;
-    const int stage_bytes = kXStage + half_n * kBK * 2;  // this CTA's share of a stage
+    const int half_n = p.bn / 2;                          // A rows per CTA per UMMA
+    const int nh = p.nh > 0 ? p.nh : 1;
+    const int y_bytes = half_n * kBK * 2;
+    const int stage_bytes = kXStage + nh * y_bytes;       // this CTA's share of a stage
+    const int bn_pair = nh * p.bn;                        // N of the pair's tile
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
     uint64_t* pfull = full + p.stages;
     uint64_t* empty = pfull + p.stages;
@@ -414,9 +418,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nkb = static_cast<int>(kb_left < p.kb_per_split ? kb_left : p.kb_per_split);
     const bool do_chain = p.do_chain != 0;
 
-    const uint32_t slot_cols = static_cast<uint32_t>((p.bn + 31) / 32 * 32);
+    // accumulator slots: double-buffered when two fit in the 512 TMEM columns
+    const uint32_t slot_cols = static_cast<uint32_t>((bn_pair + 31) / 32 * 32);
+    const int nslots = slot_cols * 2 <= 512 ? 2 : 1;
     uint32_t tmem_cols = 32;
-    while (tmem_cols < 2 * slot_cols) tmem_cols <<= 1;
+    while (tmem_cols < nslots * slot_cols) tmem_cols <<= 1;
 
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmx);
@@ -457,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int pf = p.w_prefetch;
             for (int t = pair; t < p.tiles; t += npairs) {
                 const int64_t m0 = int64_t(t / p.n_split) * (2 * kBM) + int64_t(rank) * kBM;
-                const int64_t n0 = int64_t(t % p.n_split) * p.bn + int64_t(rank) * half_n;
+                const int64_t n0 = int64_t(t % p.n_split) * bn_pair + int64_t(rank) * half_n;
                 // W streams from HBM in 128-byte row pieces: warm L2 `pf` K blocks ahead
                 for (int it = 0; it < pf && it < nkb; ++it)
                     tma_prefetch_2d(&tmx, (kb0 + it) * kBK, static_cast<int32_t>(m0));
@@ -471,7 +477,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* sy = sx + kXStage;
                     const int kc = (kb0 + it) * kBK;
                     tma_load_2d_pair(&tmx, lbar, sx, kc, static_cast<int32_t>(m0), pol_x);
-                    tma_load_2d_pair(&tmy, lbar, sy, kc, static_cast<int32_t>(n0), pol_y);
+                    for (int h = 0; h < nh; ++h)
+                        tma_load_2d_pair(&tmy, lbar, sy + h * y_bytes, kc,
+                                         static_cast<int32_t>(n0 + int64_t(h) * p.bn), pol_y);
                     if (++s == p.stages) { s = 0; ph ^= 1; }
                 }
             }
@@ -484,20 +492,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t ph = 0;
             int local = 0;
             for (int t = pair; t < p.tiles; t += npairs, ++local) {
-                const int slot = local & 1;
+                const int slot = nslots == 2 ? (local & 1) : 0;
+                const int use = nslots == 2 ? (local >> 1) : local;
                 const uint32_t tacc = tmem_base + static_cast<uint32_t>(slot) * slot_cols;
-                mbar_wait(&tmem_empty[slot], ((local >> 1) & 1) ^ 1);
+                mbar_wait(&tmem_empty[slot], (use & 1) ^ 1);
                 tc_fence_after();
                 for (int it = 0; it < nkb; ++it) {
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
                     const uint32_t sx = smem_u32(smem + s * stage_bytes);
-                    const uint32_t sy = sx + kXStage;
+                    for (int h = 0; h < nh; ++h) {
+                        const uint32_t sy = sx + kXStage + h * y_bytes;
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k) {
-                        const uint64_t ad = umma_desc_k_sw128(sx + k * 32);
-                        const uint64_t bd = umma_desc_k_sw128(sy + k * 32);
-                        umma_f16_pair(tacc, ad, bd, idesc, (it > 0 || k > 0) ? 1u : 0u);
+                        for (int k = 0; k < kBK / 16; ++k) {
+                            const uint64_t ad = umma_desc_k_sw128(sx + k * 32);
+                            const uint64_t bd = umma_desc_k_sw128(sy + k * 32);
+                            umma_f16_pair(tacc + static_cast<uint32_t>(h * p.bn), ad, bd, idesc,
+                                          (it > 0 || k > 0) ? 1u : 0u);
+                        }
                     }
                     umma_commit_pair_mc(&empty[s], 0x3);
                     if (++s == p.stages) { s = 0; ph ^= 1; }
@@ -533,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int local = 0;
         for (int t = pair; t < p.tiles; t += npairs, ++local) {
             const int64_t m0 = int64_t(t / p.n_split) * (2 * kBM) + int64_t(rank) * kBM;
-            const int64_t n0 = int64_t(t % p.n_split) * p.bn;
+            const int64_t n0 = int64_t(t % p.n_split) * bn_pair;
             const int64_t gm = m0 + row;
             if (leader && warp == 0) forward_tile(t);
             if (do_chain) {
@@ -545,13 +557,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     chain_tile<1>(cu, smem, stage_bytes, ready, empty, p.stages, local * nkb, nkb, kb0,
                                   p.chunk, m0, p.M, p.base_out, lane);
             }
-            const int slot = local & 1;
-            mbar_wait(&tmem_full[slot], (local >> 1) & 1);
+            const int slot = nslots == 2 ? (local & 1) : 0;
+            const int use = nslots == 2 ? (local >> 1) : local;
+            mbar_wait(&tmem_full[slot], use & 1);
             tc_fence_after();
             const uint32_t trow = tmem_base + static_cast<uint32_t>(slot) * slot_cols +
                                   (static_cast<uint32_t>(q * 32) << 16);
             float acc = 0.0f;
-            for (int c0 = 0; c0 < p.bn; c0 += 32) {
+            for (int c0 = 0; c0 < bn_pair; c0 += 32) {
                 uint32_t u[32];
                 tmem_ld_32x32b_x32(trow + c0, u);
                 tmem_ld_wait();
@@ -559,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __nv_bfloat16* zr = p.Z + gm * p.ldz + n0 + c0;
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
-                        if (c0 + 8 * v < p.bn && n0 + c0 + 8 * v < p.N) {
+                        if (c0 + 8 * v < bn_pair && n0 + c0 + 8 * v < p.N) {
                             float z[8];
                             unpack_bf16x8(*reinterpret_cast<const uint4*>(zr + 8 * v), z);
 #pragma unroll
@@ -575,7 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (leader) mbar_arrive(&tmem_empty[slot]);
                 else mbar_arrive_remote(mapa_shared(smem_u32(&tmem_empty[slot]), 0), 1);
             }
-            if (gm < p.M) p.out[(int64_t(ks) * p.n_split + (n0 / p.bn)) * p.M + gm] = acc;
+            if (gm < p.M) p.out[(int64_t(ks) * p.n_split + (n0 / bn_pair)) * p.M + gm] = acc;
         }
     }
     tc_fence_before();
@@ -678,12 +691,12 @@ cudaError_t launch_tc(int mode, const CUtensorMap& tx, const CUtensorMap& ty, Tc
     return cudaGetLastError();
 }
 
-size_t smem_for_pair(int bn, int stages) {
-    return size_t(stages) * (kXStage + (bn / 2) * kBK * 2) + 1024 + 256;
+size_t smem_for_pair(int bn, int stages, int nh = 1) {
+    return size_t(stages) * (kXStage + nh * (bn / 2) * kBK * 2) + 1024 + 256;
 }
 
-int stages_for_pair(int bn) {
-    const int stage = kXStage + (bn / 2) * kBK * 2;
+int stages_for_pair(int bn, int nh = 1) {
+    const int stage = kXStage + nh * (bn / 2) * kBK * 2;
     return std::min(8, (kMaxSmem - 1024 - 256) / stage);
 }
 
@@ -700,7 +713,7 @@ cudaError_t launch_tc_pair(const CUtensorMap& tx, const CUtensorMap& ty, TcParam
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs, ks, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = smem_for_pair(p.bn, p.stages);
+    cfg.dynamicSmemBytes = smem_for_pair(p.bn, p.stages, p.nh > 0 ? p.nh : 1);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -790,6 +803,7 @@ enum Strategy { kSideAll = 0, kSideGram = 1, kSerial = 2 };
 
 struct UPlan {
     bool pair;
+    int nh;         // pair kernel: UMMAs per K step (2 = full r per CTA pair, W ingested once)
     Split sp;
     int ks, kbps;
     int64_t work;   // CTAs per K split
@@ -823,6 +837,26 @@ UPlan plan_u(int64_t d_out, int64_t r, int64_t kb_in, int64_t chunk_blocks, int6
     u.ctas = static_cast<int>(std::min<int64_t>(u.work * u.ks, budget));
     u.cycles = u.pair ? gemm_cycles(pm_tiles * u.sp.ns * u.ks, std::max(1, u.ctas / 2), u.kbps, u.sp.bn)
                       : gemm_cycles(u.work * u.ks, std::max(1, u.ctas), u.kbps, u.sp.bn);
+    u.nh = 1;
+    // Full r per CTA pair (two UMMAs of N = r/2 per K step): W is ingested by one pair
+    // instead of one per N split, at twice the MMA work per SM.  On a full GPU the N-split
+    // tiling is faster; under an SM budget (dfx_ctx_set_sm_budget, compose kernels running
+    // beside the norm) the one-pass tiling wins once the N splits would need a second round.
+    const int64_t bnh = ((r + 1) / 2 + 31) / 32 * 32;
+    if (u.pair && r > 256 && 2 * bnh <= 512 && u.sp.ns > 1) {
+        const int pairs = std::max(1, budget / 2);
+        const int64_t kbps1 = int64_t(chunks_per_split) * chunk_blocks;
+        const double c1 = gemm_cycles(pm_tiles * u.ks, pairs, kbps1, static_cast<int>(bnh)) +
+                          double((pm_tiles * u.ks + pairs - 1) / pairs) * double(kbps1) * 4.0 *
+                              std::max(120.0, 0.5 * double(bnh));
+        if (c1 <= u.cycles) {
+            u.nh = 2;
+            u.sp = {1, u.sp.ks, static_cast<int>(bnh)};
+            u.work = 2 * pm_tiles;
+            u.ctas = static_cast<int>(std::min<int64_t>(u.work * u.ks, budget));
+            u.cycles = c1;
+        }
+    }
     return u;
 }
 
@@ -952,7 +986,8 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
             // A box = half of the pair's BN rows (each CTA of the pair loads its half)
             e = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, u.sp.bn / 2, true);
             if (e != cudaSuccess) return e;
-            p.stages = stages_for_pair(u.sp.bn);
+            p.nh = u.nh;
+            p.stages = stages_for_pair(u.sp.bn, u.nh);
             p.tiles = static_cast<int>(pm_tiles * u.sp.ns);
             const int pairs = std::min<int>(p.tiles, std::max(1, u.ctas / (2 * u.ks)));
             e = launch_tc_pair(tw, ta, p, pairs, u.ks, st, "u_rowdot_tc");

@@ -230,3 +230,50 @@ def test_invalid_arguments(dfx):
         dfx.norm_terms(w, a[:0], b, 1.0, 16, o, o, o)       # rank 0
     with pytest.raises(P.DfxInvalidArgument):
         dfx.norm_terms(w, a, b, 1.0, 0, o, o, o)            # bad chunk plan
+
+
+@pytest.mark.parametrize("budget", [64, 24, 8])
+@pytest.mark.parametrize("d_out,d_in,r", [(1024, 1024, 384), (128, 4096, 512), (2048, 2048, 384),
+                                          (768, 4608, 320)])
+def test_sm_budget_plans(oracle, budget, d_out, d_in, r):
+    """dfx_ctx_set_sm_budget re-plans the norm GEMMs (a budget below two N-split rounds picks
+    the full-r 2-SM tiling, two UMMAs per K step, W ingested once); the result keeps the
+    same bar: base_sq bitwise, cross / ba_sq within the fp32 bound, norm within a bf16 ulp."""
+    import paper_2603_22276_b200 as P
+    dfx = P.Dfx(0)
+    dfx.set_sm_budget(budget)
+    W, A, B = _fixture(oracle, d_out, d_in, r, 17 * d_out + r + budget, dt=1)
+    s = 2.0 / np.sqrt(r)
+    cs, _ = oracle.plan_chunks(d_out, d_in)
+    want = oracle.norm_terms(W, A, B, s, cs)
+    m = np.abs(oracle.gaussian_vector(d_out, 1.0, 0.1, 5))
+    wn, g, t = _row_norm(dfx, W, A, B, s, cs, 1, m=m)
+    assert bits_equal(t[0], want[0])
+    scale_c = np.sqrt(want[0] * np.abs(want[2])) + 1e-30
+    assert np.all(np.abs(t[1] - want[1]) <= 2e-5 * scale_c + 1e-6 * np.abs(want[1]))
+    assert np.all(np.abs(t[2] - want[2]) <= 1e-4 * np.abs(want[2]) + 1e-6 * want[2].max())
+    want_n = oracle.row_norm(1, W, A, B, s, cs)
+    assert np.all(np.abs(wn - want_n) <= np.spacing(want_n.astype(np.float32)) * 2 ** 16)
+    dfx.close()
+
+
+def test_sm_budget_full_size_c2(oracle):
+    """C2 at full size under the pipelined bench's budget: base_sq bitwise on every row."""
+    import paper_2603_22276_b200 as P
+    dfx = P.Dfx(0)
+    dfx.set_sm_budget(72)
+    d_out = d_in = 8192
+    r = 384
+    rng = np.random.default_rng(7)
+    W = to_np(to_dev(rng.standard_normal((d_out, d_in), dtype=np.float32), 1))
+    A = to_np(to_dev(rng.standard_normal((r, d_in), dtype=np.float32), 1))
+    B = to_np(to_dev(rng.standard_normal((d_out, r), dtype=np.float32), 1))
+    s = 2.0 / np.sqrt(r)
+    cs, _ = oracle.plan_chunks(d_out, d_in)
+    t = np.stack(_terms(dfx, W, A, B, s, cs, 1))
+    assert bits_equal(t[0], oracle.norm_terms(W, A, B, 0.0, cs)[0])
+    rows = np.sort(rng.choice(d_out, 128, replace=False))
+    sub = oracle.norm_terms(np.ascontiguousarray(W[rows]), A, np.ascontiguousarray(B[rows]), s, cs)
+    assert np.all(np.abs(t[1][rows] - sub[1]) <= 2e-5 * np.sqrt(sub[0] * sub[2]))
+    assert np.all(np.abs(t[2][rows] - sub[2]) <= 1e-4 * sub[2])
+    dfx.close()

@@ -85,6 +85,31 @@ template <> struct Vec<__half> {
     }
 };
 
+// one 32-bit shared-memory word -> its 1 (fp32) or 2 (16-bit) values
+template <typename T> struct Word;
+template <> struct Word<float> {
+    static __device__ __forceinline__ void unpack(uint32_t w, float (&f)[1]) { f[0] = __uint_as_float(w); }
+};
+template <> struct Word<__nv_bfloat16> {
+    static __device__ __forceinline__ void unpack(uint32_t w, float (&f)[2]) {
+        f[0] = __uint_as_float(w << 16);
+        f[1] = __uint_as_float(w & 0xFFFF0000u);
+    }
+};
+template <> struct Word<__half> {
+    static __device__ __forceinline__ void unpack(uint32_t w, float (&f)[2]) {
+        const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&w));
+        f[0] = v.x;
+        f[1] = v.y;
+    }
+};
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -226,7 +251,8 @@ struct SerialCfg {
     static constexpr int kRB = 64;                          // rows per stage
     static constexpr int kStages = 6;
     static constexpr int kStageBytes = kRB * 128;           // per tensor
-    static constexpr int kChainWarps = kSC / 32;            // 2 (16-bit) or 1 (fp32)
+    static constexpr int kCPT = 4 / sizeof(T);              // chain columns per thread
+    static constexpr int kChainWarps = 1;                   // 32 threads x kCPT columns
     static constexpr int kEltWarps = 4;
     static constexpr int kThreads = 32 * (1 + kChainWarps + kEltWarps);
     static constexpr int kSmem = 2 * kStages * kStageBytes + 2 * kStages * 8 + 1024;
@@ -277,42 +303,57 @@ __global__ void __launch_bounds__(SerialCfg<T>::kThreads, 1)
             }
         }
     } else if (warp <= C::kChainWarps) {
-        // chain thread: column j, serial fp32 acc over rows ascending
-        const int jc = (warp - 1) * 32 + lane;
-        float acc = 0.0f;
+        // chain thread: kCPT adjacent columns (one 32-bit shared-memory word per row), one
+        // serial fp32 accumulator per column over rows ascending (independent chains)
+        constexpr int P = C::kCPT;
+        const int jc = lane * P;
+        float acc[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) acc[c] = 0.0f;
         for (int it = 0; it < n_iter; ++it) {
             const int s = it % C::kStages;
             mbar_wait(&full[s], (it / C::kStages) & 1);
-            const T* py = reinterpret_cast<const T*>(s_dy + s * C::kStageBytes) + jc;
-            const T* pi = reinterpret_cast<const T*>(s_in + s * C::kStageBytes) + jc;
+            const uint32_t py = smem_u32(s_dy + s * C::kStageBytes) + jc * sizeof(T);
+            const uint32_t pi = smem_u32(s_in + s * C::kStageBytes) + jc * sizeof(T);
             const int64_t rem = rows - int64_t(it) * C::kRB;
             const int nr = rem < C::kRB ? static_cast<int>(rem) : C::kRB;
             if (nr == C::kRB) {
-                // Full stage: load a batch of 16 rows into registers, form the 16
-                // (independent) products, then run the dependent adds in row order, so
+                // Full stage: a batch of 16 rows is loaded first, the (independent)
+                // products formed, then the dependent adds run in row order, so the
                 // shared-memory latency is paid once per batch, not once per row.
 #pragma unroll
                 for (int i0 = 0; i0 < C::kRB; i0 += 16) {
-                    float p[16];
+                    float p[16][P];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        float fy[P], fi[P];
+                        Word<T>::unpack(lds_u32(py + (i0 + u) * 128), fy);
+                        Word<T>::unpack(lds_u32(pi + (i0 + u) * 128), fi);
+#pragma unroll
+                        for (int c = 0; c < P; ++c) p[u][c] = __fmul_rn(fy[c], fi[c]);
+                    }
 #pragma unroll
                     for (int u = 0; u < 16; ++u)
-                        p[u] = __fmul_rn(Elem<T>::to_f(py[(i0 + u) * C::kSC]),
-                                         Elem<T>::to_f(pi[(i0 + u) * C::kSC]));
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) acc = __fadd_rn(acc, p[u]);
+                        for (int c = 0; c < P; ++c) acc[c] = __fadd_rn(acc[c], p[u][c]);
                 }
             } else {
                 for (int i = 0; i < nr; ++i) {
-                    const float p = __fmul_rn(Elem<T>::to_f(py[i * C::kSC]),
-                                              Elem<T>::to_f(pi[i * C::kSC]));
-                    acc = __fadd_rn(acc, p);
+                    float fy[P], fi[P];
+                    Word<T>::unpack(lds_u32(py + i * 128), fy);
+                    Word<T>::unpack(lds_u32(pi + i * 128), fi);
+#pragma unroll
+                    for (int c = 0; c < P; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(fy[c], fi[c]));
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
         }
-        const int64_t j = col0 + jc;
-        if (j < d_out) d_mag[j] = __fdiv_rn(acc, __ldg(w_norm + j));
+#pragma unroll
+        for (int c = 0; c < P; ++c) {
+            const int64_t j = col0 + jc + c;
+            if (j < d_out) d_mag[j] = __fdiv_rn(acc[c], __ldg(w_norm + j));
+        }
     } else {
         // elementwise warps: 128 threads, each a fixed 16-byte column vector
         const int t = threadIdx.x - 32 * (1 + C::kChainWarps);

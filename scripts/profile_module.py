@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--bwd", action="store_true")
+    ap.add_argument("--budget", type=int, default=0, help="dfx_ctx_set_sm_budget for the norm")
     a = ap.parse_args()
     import torch
     import paper_2603_22276_b200 as P
@@ -22,6 +23,7 @@ def main():
     d_out, d_in, r, rows = cfg["d_out"], cfg["d_in"], cfg["r"], cfg["tokens"]
     s = 2.0 / math.sqrt(r)
     dfx = P.Dfx(0)
+    dfx.set_sm_budget(a.budget)
     cs, _ = P.plan_chunks(d_out, d_in)
     bf = torch.bfloat16
     W = torch.randn(d_out, d_in, device="cuda").to(bf)

@@ -469,7 +469,9 @@ def run_gpu(args, rank, world, local_rank, dist):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(args.config, {}).get(dom)
+            tr = json.load(f).get(args.config, {})
+            budget_key = f"{dom}_budget{args.norm_sms}"
+            traffic = tr.get(budget_key if (args.pipeline > 1 and budget_key in tr) else dom)
     except Exception:
         pass
     dk = kernels[dom]

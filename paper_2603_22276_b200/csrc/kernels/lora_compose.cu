@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
     uint64_t* tmem_empty = tmem_full + 2;        // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
-    __shared__ __align__(16) float s_gb[2][2][128];   // epilogue: [group][g | bias][column]
+    __shared__ __align__(16) float s_gw[8][3][kLN / 2];   // epilogue warp: g, g - 1, bias
     const int warp = warp_id(), lane = lane_id();
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.stages; ++i) {
@@ -204,15 +204,17 @@ __global__ void __launch_bounds__(kLThreads, 1)
         }
     } else if (warp < 8) {
         // ================= epilogue: one token row per thread =================
-        // Group grp (warps 4*grp .. 4*grp+3) owns columns [128*grp, 128*grp + 128) of each
-        // tile, in four 32-column slices; each slice's outputs go to a double-buffered
-        // 64-byte-swizzled smem tile and leave by TMA store while the next slice computes.
+        // Warp w (TMEM lane quadrant q = w % 4) owns the 32 rows 32q.. of each tile and the
+        // column half grp = w / 4, in four 32-column slices.  Each slice's outputs go to the
+        // warp's part of a double-buffered 64-byte-swizzled smem slice and leave by the
+        // warp's own TMA store (32 x 32 box) while the next slice computes: no cross-warp
+        // synchronisation in the epilogue.
         const int grp = warp >> 2, q = warp & 3;
         const int row = q * 32 + lane;
         const int sw = (row >> 1) & 3;                          // SWIZZLE_64B chunk XOR
         uint8_t* obase = s_out + grp * 2 * p.n_out * kSlice;    // [2 buffers][n_out][slice]
+        float (*gw)[kLN / 2] = s_gw[warp];                      // [g | g - 1 | bias][column]
         const float sf = p.s;
-        const bool issuer = q == 0 && lane == 0;
         // this thread's 64-byte base piece of a slice (row clamped in the token tail, columns
         // in the d_out tail; those outputs are clipped by the TMA store), read through L1
         // one slice ahead so the DRAM latency hides behind the current slice's arithmetic
@@ -230,15 +232,20 @@ __global__ void __launch_bounds__(kLThreads, 1)
         int local = 0, nslice = 0;
         for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++local) {
             const int32_t m0 = (t % p.m_tiles) * kLM, n0 = (t / p.m_tiles) * kLN;
-            // the group's 128 columns of g and bias, staged once per tile (a missing bias
-            // is -0.0, an exact no-op in the fp32 add); columns past d_out are clamped,
-            // their outputs are clipped by the TMA store
+            // g, g - 1 and bias for the warp's 128 columns (a missing bias is -0.0, an exact
+            // no-op in the fp32 add; columns past d_out are clamped, their outputs clipped)
             {
-                const int64_t j = min(int64_t(n0 + 128 * grp + row), p.d_out - 1);
-                s_gb[grp][0][row] = __ldg(p.g + j);
-                s_gb[grp][1][row] = p.bias ? __ldg(p.bias + j) : -0.0f;
+                const int64_t j = min(int64_t(n0 + 128 * grp + 4 * lane), p.d_out - 4);
+                const float4 gv4 = __ldg(reinterpret_cast<const float4*>(p.g + j));
+                const float4 bv4 = p.bias ? __ldg(reinterpret_cast<const float4*>(p.bias + j))
+                                          : make_float4(-0.0f, -0.0f, -0.0f, -0.0f);
+                reinterpret_cast<float4*>(gw[0])[lane] = gv4;
+                reinterpret_cast<float4*>(gw[1])[lane] =
+                    make_float4(__fsub_rn(gv4.x, 1.0f), __fsub_rn(gv4.y, 1.0f),
+                                __fsub_rn(gv4.z, 1.0f), __fsub_rn(gv4.w, 1.0f));
+                reinterpret_cast<float4*>(gw[2])[lane] = bv4;
             }
-            named_bar_sync(1 + grp, 128);
+            __syncwarp();
             const int slot = local & 1;
             mbar_wait(&tmem_full[slot], (local >> 1) & 1);
             tc_fence_after();
@@ -260,18 +267,19 @@ __global__ void __launch_bounds__(kLThreads, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tmem_empty[slot]);
                 }
-                const uint32_t orow = smem_u32(obase + (nslice & 1) * p.n_out * kSlice) +
-                                      static_cast<uint32_t>(row * (kLSlice * 2));
-                float4 gq[8], bq[8];                         // the slice's 32 g / bias values
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    gq[k] = reinterpret_cast<const float4*>(&s_gb[grp][0][kLSlice * cs])[k];
-                    bq[k] = reinterpret_cast<const float4*>(&s_gb[grp][1][kLSlice * cs])[k];
-                }
+                uint8_t* obuf = obase + (nslice & 1) * p.n_out * kSlice;
+                const uint32_t orow = smem_u32(obuf) + static_cast<uint32_t>(row * (kLSlice * 2));
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {                 // 8 columns per 16-byte chunk
-                    const float4 g0 = gq[2 * k], g1 = gq[2 * k + 1], b0 = bq[2 * k], b1 = bq[2 * k + 1];
+                    const int c8 = kLSlice * cs + 8 * k;        // column within the warp's half
+                    const float4 g0 = *reinterpret_cast<const float4*>(&gw[0][c8]);
+                    const float4 g1 = *reinterpret_cast<const float4*>(&gw[0][c8 + 4]);
+                    const float4 h0 = *reinterpret_cast<const float4*>(&gw[1][c8]);
+                    const float4 h1 = *reinterpret_cast<const float4*>(&gw[1][c8 + 4]);
+                    const float4 b0 = *reinterpret_cast<const float4*>(&gw[2][c8]);
+                    const float4 b1 = *reinterpret_cast<const float4*>(&gw[2][c8 + 4]);
                     const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+                    const float gm[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
                     const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
                     const uint32_t bw[4] = {bv[k].x, bv[k].y, bv[k].z, bv[k].w};
                     // element pairs: every dtype rounding is one packed F2FP conversion of
@@ -286,8 +294,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
                         const float l0 = LcT<T>::lo(lw), l1 = LcT<T>::hi(lw);
                         const float t0 = __fmul_rn(sf, l0), t1 = __fmul_rn(sf, l1);
                         const float u0 = __fmul_rn(gv[e], t0), u1 = __fmul_rn(gv[e + 1], t1);
-                        const float v0 = __fmul_rn(__fsub_rn(gv[e], 1.0f), b0f);
-                        const float v1 = __fmul_rn(__fsub_rn(gv[e + 1], 1.0f), b1f);
+                        const float v0 = __fmul_rn(gm[e], b0f), v1 = __fmul_rn(gm[e + 1], b1f);
                         const uint32_t dw = LcT<T>::pack(__fadd_rn(v0, u0), __fadd_rn(v1, u1));
                         const uint32_t y0w = LcT<T>::pack(__fadd_rn(b0f, LcT<T>::lo(dw)),
                                                           __fadd_rn(b1f, LcT<T>::hi(dw)));
@@ -305,22 +312,22 @@ __global__ void __launch_bounds__(kLThreads, 1)
                                o[kind][0], o[kind][1], o[kind][2], o[kind][3]);
                     }
                 }
-                // hand the slice to the TMA store; the issuer then waits until the store of
-                // the previous slice (the other buffer) has read its smem, so after the
-                // barrier the next slice may overwrite that buffer
+                // the warp's 32 rows of the slice go out by its own TMA store; before the
+                // next slice reuses the other buffer, the store issued from it two slices
+                // ago must have read its smem
                 fence_async_smem();
-                named_bar_sync(1 + grp, 128);
-                if (issuer) {
+                __syncwarp();
+                if (lane == 0) {
                     for (int oi = 0; oi < p.n_out; ++oi)
-                        tma_store_2d(&maps.out[oi], obase + ((nslice & 1) * p.n_out + oi) * kSlice,
-                                     col0, m0);
+                        tma_store_2d(&maps.out[oi], obuf + oi * kSlice + q * 32 * (kLSlice * 2),
+                                     col0, m0 + 32 * q);
                     bulk_commit();
                     bulk_wait_read1();
                 }
-                named_bar_sync(1 + grp, 128);
+                __syncwarp();
             }
         }
-        if (q == 0 && lane == 0) bulk_wait0();
+        if (lane == 0) bulk_wait0();
     }
     tc_fence_before();
     __syncthreads();
@@ -349,7 +356,7 @@ cudaError_t launch_lora_compose(int dt, const void* mid, const void* b, const vo
         p.slot[k] = -1;
         if (!outs[k]) continue;
         cudaError_t e = make_tmap_2d_sw(&maps.out[p.n_out], dt, outs[k], rows, d_out, d_out * 2,
-                                        kLSlice, kLM, 64);
+                                        kLSlice, 32, 64);      // one warp's 32 rows
         if (e != cudaSuccess) return e;
         p.slot[k] = p.n_out++;
     }

@@ -652,7 +652,7 @@ def main():
     ap.add_argument("--prof-steps", type=int, default=40)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--pipeline", type=int, default=8,
+    ap.add_argument("--pipeline", type=int, default=40,
                     help="modules per graph, software-pipelined on two streams (1 = serial)")
     ap.add_argument("--mode", default="train", choices=["train", "infer"],
                     help="train: norm + dual compose + backward (headline); infer: norm + compose")

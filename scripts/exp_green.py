@@ -22,6 +22,7 @@ def main():
     import paper_2603_22276_b200 as P
     norm_sms = int(sys.argv[1]) if len(sys.argv) > 1 else 64
     budget = int(sys.argv[2]) if len(sys.argv) > 2 else norm_sms
+    only = sys.argv[3] if len(sys.argv) > 3 else "both"     # both | norm | compose
     torch.cuda.init()
     torch.zeros(1, device="cuda")
     chk(drv.cuInit(0))
@@ -68,13 +69,16 @@ def main():
             with torch.cuda.stream(tsA):
                 if i >= nb:
                     tsA.wait_event(evc[i - nb])
-                dfx.row_norm(b["W"], b["A"], b["B"], s, cs, b["wn"], m=b["m"], g=b["g"], stream=tsA)
+                if only in ("both", "norm"):
+                    dfx.row_norm(b["W"], b["A"], b["B"], s, cs, b["wn"], m=b["m"], g=b["g"], stream=tsA)
                 evn[i].record(tsA)
             with torch.cuda.stream(tsB):
                 tsB.wait_event(evn[i])
-                dfx.compose_fwd(b["base"], b["lora"], b["g"], s, b["delta"], b["inner"], stream=tsB)
-                dfx.compose_bwd(b["dy"], b["g"], s, b["dl"], b["db"], inner=b["inner"], w_norm=b["wn"],
-                                d_mag=b["dm"], stream=tsB)
+                if only in ("both", "compose", "dual"):
+                    dfx.compose_fwd(b["base"], b["lora"], b["g"], s, b["delta"], b["inner"], stream=tsB)
+                if only in ("both", "compose", "bwd"):
+                    dfx.compose_bwd(b["dy"], b["g"], s, b["dl"], b["db"], inner=b["inner"], w_norm=b["wn"],
+                                    d_mag=b["dm"], stream=tsB)
                 evc[i].record(tsB)
         return evc[n - 1]
 
@@ -89,7 +93,7 @@ def main():
     e1.record(tsA)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    print(f"norm_sms={norm_sms} budget={budget}: {ms / n * 1e3:.1f} us/module, {n / ms * 1e3:.0f} modules/s")
+    print(f"{only} norm_sms={norm_sms} budget={budget}: {ms / n * 1e3:.1f} us/module, {n / ms * 1e3:.0f} modules/s")
 
 
 if __name__ == "__main__":

@@ -40,6 +40,10 @@ cudaError_t launch_finish(const FinishArgs& f, cudaStream_t st);
 // shape/dtype is outside the TMA/UMMA envelope so the caller can use the SIMT path.
 cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, int* launches);
 bool norm_tc_supported(int dt, int64_t d_out, int64_t d_in, int64_t r);
+// fp32 weights on the tensor cores (3xTF32); DFX_NORM_TF32=0 keeps them on the SIMT path.
+bool norm_tc_f32_supported(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk);
+bool norm_tf32_enabled();
+cudaError_t launch_norm_tc_f32(const NormArgs& a, Workspace* ws, cudaStream_t st, int* launches);
 
 // The stored value of round_to_dtype(x) for x already fp32 (dtype.cpp:77-85):
 // RNE to the target grid, result kept in fp32 storage.

@@ -324,6 +324,7 @@ cudaError_t launch_magnitude_scale(int dt, const float* m, const float* w_norm, 
 }
 
 int norm_uses_tensor_cores(int dt, int64_t d_out, int64_t d_in, int64_t r) {
+    if (dt == kF32) return norm_tf32_enabled() && norm_tc_f32_supported(d_out, d_in, r, 32) ? 1 : 0;
     return norm_tc_supported(dt, d_out, d_in, r) ? 1 : 0;
 }
 
@@ -334,6 +335,9 @@ cudaError_t launch_norm(const NormArgs& a, Workspace* ws, cudaStream_t st, int* 
     if ((a.s != 0.0 || a.mode == kNormPartial) && a.chunk_size % 64 == 0 &&
         norm_tc_supported(a.dt, a.d_out, tc_din, a.r))
         return launch_norm_tc(a, ws, st, launches);
+    if (a.dt == kF32 && a.s != 0.0 && a.mode == kNormFull && norm_tf32_enabled() &&
+        norm_tc_f32_supported(a.d_out, a.d_in, a.r, a.chunk_size))
+        return launch_norm_tc_f32(a, ws, st, launches);
     switch (a.dt) {
         case kF32: return norm_simt_impl<float>(a, ws, st, launches);
         case kBF16: return norm_simt_impl<__nv_bfloat16>(a, ws, st, launches);

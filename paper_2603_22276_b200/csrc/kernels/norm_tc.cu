@@ -51,7 +51,7 @@ struct TcParams {
     int x_kwrap;            // X k coordinate wraps modulo this (ba_sq: r_pad); 0 = none
     int64_t chunk;          // ChunkPlan chunk size (chain), multiple of 64
     // rowdot
-    const __nv_bfloat16* Z; int64_t ldz;
+    const void* Z; int64_t ldz;   // bf16, or fp32 in the 3xTF32 kernel
     float* out;             // rowdot: [k_split*n_split][M]; store: tiles
     float* base_out;        // chain: [num_chunks][M], one serial partial per chunk
     int do_chain;
@@ -101,7 +101,7 @@ __device__ __forceinline__ int chain_active_warps(int n_idx, int n_split) {
 // ChainPlan chunk (factored_norm.cpp:52-60); partials go to base_out[chunk][row] and the
 // finisher adds them in ascending order (:60), so base_sq is bitwise the reference's.
 // The stage is released only after the chain consumed its registers.
-template <int kRows>
+template <int kRows, bool kF32 = false>
 __device__ __forceinline__ void chain_tile(const ChainUnits& cu, const uint8_t* smem,
                                            int stage_bytes, uint64_t* ready, uint64_t* empty,
                                            int stages, int start, int nkb, int kb0, int64_t chunk,
@@ -115,7 +115,7 @@ __device__ __forceinline__ void chain_tile(const ChainUnits& cu, const uint8_t* 
         part[j] = 0.0f;
         row[j] = 32 * cu.u[j] + lane;
     }
-    int64_t kpos = int64_t(kb0) * 64;
+    int64_t kpos = int64_t(kb0) * (kF32 ? 32 : 64);
     int64_t cur = kpos / chunk;
     int64_t boundary = (cur + 1) * chunk;
     for (int it = 0; it < nkb; ++it) {
@@ -139,18 +139,26 @@ __device__ __forceinline__ void chain_tile(const ChainUnits& cu, const uint8_t* 
         }
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
+            constexpr int kE = kF32 ? 4 : 8;               // elements per 16-byte chunk
             float f[kRows][8];
 #pragma unroll
-            for (int j = 0; j < kRows; ++j) unpack_bf16x8(v[j][c], f[j]);
+            for (int j = 0; j < kRows; ++j) {
+                if (kF32) {
+                    f[j][0] = __uint_as_float(v[j][c].x); f[j][1] = __uint_as_float(v[j][c].y);
+                    f[j][2] = __uint_as_float(v[j][c].z); f[j][3] = __uint_as_float(v[j][c].w);
+                } else {
+                    unpack_bf16x8(v[j][c], f[j]);
+                }
+            }
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
+            for (int e = 0; e < kE; ++e)
 #pragma unroll
                 for (int j = 0; j < kRows; ++j)
                     part[j] = __fadd_rn(part[j], __fmul_rn(f[j][e], f[j][e]));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        kpos += 64;
+        kpos += kF32 ? 32 : 64;
         if (++s == stages) { s = 0; ph ^= 1; }
     }
 #pragma unroll
@@ -176,7 +184,12 @@ __device__ __forceinline__ void tile_coords(int kMode, const TcParams& p, int t,
 // Persistent: CTA b walks tiles b, b + gridDim.x, ...; the smem stage ring and its
 // phases run on across tiles, and the TMEM accumulator is double-buffered (2 x BN
 // columns) so the MMA of tile i+1 overlaps the epilogue of tile i.
-template <int kMode>
+// kF32: the 3xTF32 variant for fp32 operands.  A K block is 32 fp32 (the same 128-byte
+// swizzle row); two split warps write each stage's low parts x - tf32(x) next to the raw
+// tiles, and every K=8 step issues three kind::tf32 UMMAs, X.Y + X.Y_lo + X_lo.Y (the raw
+// fp32 operand is read as its TF32 truncation), which carries ~2^-21 relative error —
+// fp32-class accumulation on the tensor cores.
+template <int kMode, bool kF32 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_rowdot(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
               const TcParams p) {
@@ -184,17 +197,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     const int y_stage = p.bn * kBK * 2;
-    const int stage_bytes = kXStage + y_stage;  // both multiples of 1024
+    const int raw_bytes = kXStage + y_stage;    // both multiples of 1024
+    const int stage_bytes = kF32 ? 2 * raw_bytes : raw_bytes;   // [raw X | raw Y | lo X | lo Y]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
     uint64_t* empty = full + p.stages;
     uint64_t* tmem_full = empty + p.stages;     // [2]
     uint64_t* tmem_empty = tmem_full + 2;       // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    uint64_t* split = tmem_empty + 2;           // [stages] (kF32: low parts written)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(split + p.stages);
 
     const int warp = warp_id(), lane = lane_id();
     const int ks = blockIdx.y;
     const int kb0 = ks * p.kb_per_split;
-    const int64_t total_kb = (p.k_total + kBK - 1) / kBK;
+    constexpr int kBKe = kF32 ? 32 : kBK;       // K elements per 128-byte block
+    const int64_t total_kb = (p.k_total + kBKe - 1) / kBKe;
     const int64_t kb_left = total_kb - kb0;
     const int nkb = static_cast<int>(kb_left < p.kb_per_split ? kb_left : p.kb_per_split);
     const bool do_chain = (kMode == kTcRowdot) && p.do_chain;
@@ -215,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tmem_full[a], 1);
             mbar_init(&tmem_empty[a], 4);
         }
+        for (int s = 0; s < p.stages; ++s) mbar_init(&split[s], 2);
         fence_mbar_init();
     }
     if (warp == kWarpMma) {
@@ -250,10 +267,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (it + pf < nkb)
                         tma_prefetch_2d(&tmx, (kb0 + it + pf) * kBK, static_cast<int32_t>(m0));
                     mbar_wait(&empty[s], ph ^ 1);
-                    mbar_arrive_expect_tx(&full[s], stage_bytes);
+                    mbar_arrive_expect_tx(&full[s], raw_bytes);
                     uint8_t* sx = smem + s * stage_bytes;
                     uint8_t* sy = sx + kXStage;
-                    const int kc = (kb0 + it) * kBK;
+                    const int kc = (kb0 + it) * (kF32 ? 32 : kBK);
                     const int kx = (p.x_kwrap && kc >= p.x_kwrap) ? kc - p.x_kwrap : kc;
                     tma_load_2d(&tmx, &full[s], sx, kx, static_cast<int32_t>(m0), pol_x);
                     tma_load_2d(&tmy, &full[s], sy, kc, static_cast<int32_t>(n0), pol_y);
@@ -264,7 +281,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (nkb > 0 && warp == kWarpMma) {
         // ================= MMA issuer (single thread) =================
         if (lane == 0) {
-            const uint32_t idesc = umma_idesc_f16(1u, kBM, static_cast<uint32_t>(p.bn));
+            const uint32_t idesc = kF32 ? umma_idesc_tf32(kBM, static_cast<uint32_t>(p.bn))
+                                        : umma_idesc_f16(1u, kBM, static_cast<uint32_t>(p.bn));
             int s = 0;
             uint32_t ph = 0;
             int local = 0;
@@ -277,15 +295,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&tmem_empty[slot], ((local >> 1) & 1) ^ 1);
                 tc_fence_after();
                 for (int it = 0; it < nkb; ++it) {
-                    mbar_wait(&full[s], ph);
+                    mbar_wait(kF32 ? &split[s] : &full[s], ph);
                     tc_fence_after();
                     const uint32_t sx = smem_u32(smem + s * stage_bytes);
                     const uint32_t sy = sx + kXStage;
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k) {
+                    for (int k = 0; k < 4; ++k) {
                         const uint64_t ad = umma_desc_k_sw128(sx + k * 32);
                         const uint64_t bd = umma_desc_k_sw128(sy + k * 32);
-                        umma_f16(tacc, ad, bd, idesc, (it > 0 || k > 0) ? 1u : 0u);
+                        if (kF32) {
+                            const uint64_t adl = umma_desc_k_sw128(sx + raw_bytes + k * 32);
+                            const uint64_t bdl = umma_desc_k_sw128(sy + raw_bytes + k * 32);
+                            umma_tf32(tacc, ad, bd, idesc, (it > 0 || k > 0) ? 1u : 0u);
+                            umma_tf32(tacc, ad, bdl, idesc, 1u);
+                            umma_tf32(tacc, adl, bd, idesc, 1u);
+                        } else {
+                            umma_f16(tacc, ad, bd, idesc, (it > 0 || k > 0) ? 1u : 0u);
+                        }
                     }
                     umma_commit(&empty[s]);
                     // stand in for the epilogue warps that do not chain in this tile
@@ -293,6 +319,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (++s == p.stages) { s = 0; ph ^= 1; }
                 }
                 umma_commit(&tmem_full[slot]);
+            }
+        }
+    } else if (kF32 && nkb > 0 && warp >= 6) {
+        // ================= 3xTF32 split: low parts x - tf32(x) of both tiles ==========
+        const int st = (warp - 6) * 32 + lane;                  // 0 .. 63
+        int s = 0;
+        uint32_t ph = 0;
+        for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+            for (int it = 0; it < nkb; ++it) {
+                mbar_wait(&full[s], ph);
+                const uint4* src = reinterpret_cast<const uint4*>(smem + s * stage_bytes);
+                uint4* dst = reinterpret_cast<uint4*>(smem + s * stage_bytes + raw_bytes);
+                for (int i = st; i < raw_bytes / 16; i += 64) {
+                    const uint4 w = src[i];
+                    uint4 l;
+                    l.x = __float_as_uint(__fsub_rn(__uint_as_float(w.x), __uint_as_float(w.x & 0xFFFFE000u)));
+                    l.y = __float_as_uint(__fsub_rn(__uint_as_float(w.y), __uint_as_float(w.y & 0xFFFFE000u)));
+                    l.z = __float_as_uint(__fsub_rn(__uint_as_float(w.z), __uint_as_float(w.z & 0xFFFFE000u)));
+                    l.w = __float_as_uint(__fsub_rn(__uint_as_float(w.w), __uint_as_float(w.w & 0xFFFFE000u)));
+                    dst[i] = l;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&split[s]);
+                if (++s == p.stages) { s = 0; ph ^= 1; }
             }
         }
     } else if (nkb > 0 && warp < 4) {
@@ -307,11 +358,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (do_chain) {
                 const ChainUnits cu = chain_units(warp, static_cast<int>(t % p.n_split), p.n_split);
                 if (cu.n == 2)
-                    chain_tile<2>(cu, smem, stage_bytes, full, empty, p.stages, local * nkb, nkb, kb0,
-                                  p.chunk, m0, p.M, p.base_out, lane);
+                    chain_tile<2, kF32>(cu, smem, stage_bytes, full, empty, p.stages, local * nkb, nkb,
+                                        kb0, p.chunk, m0, p.M, p.base_out, lane);
                 else if (cu.n == 1)
-                    chain_tile<1>(cu, smem, stage_bytes, full, empty, p.stages, local * nkb, nkb, kb0,
-                                  p.chunk, m0, p.M, p.base_out, lane);
+                    chain_tile<1, kF32>(cu, smem, stage_bytes, full, empty, p.stages, local * nkb, nkb,
+                                        kb0, p.chunk, m0, p.M, p.base_out, lane);
             }
             // ---- epilogue: TMEM accumulator -> rowdot / tile store
             const int slot = local & 1;
@@ -326,13 +377,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_ld_32x32b_x32(trow + c0, u);
                     tmem_ld_wait();
                     if (gm < p.M) {
-                        const __nv_bfloat16* zr = p.Z + gm * p.ldz + n0 + c0;
 #pragma unroll
                         for (int v = 0; v < 4; ++v) {
                             // columns past the tile (bn % 32 != 0) belong to the other slot
                             if (c0 + 8 * v < p.bn && n0 + c0 + 8 * v < p.N) {
                                 float z[8];
-                                unpack_bf16x8(*reinterpret_cast<const uint4*>(zr + 8 * v), z);
+                                if (kF32) {
+                                    const float* zr = static_cast<const float*>(p.Z) + gm * p.ldz + n0 + c0;
+                                    const float4 z0 = *reinterpret_cast<const float4*>(zr + 8 * v);
+                                    const float4 z1 = *reinterpret_cast<const float4*>(zr + 8 * v + 4);
+                                    z[0] = z0.x; z[1] = z0.y; z[2] = z0.z; z[3] = z0.w;
+                                    z[4] = z1.x; z[5] = z1.y; z[6] = z1.z; z[7] = z1.w;
+                                } else {
+                                    const __nv_bfloat16* zr =
+                                        static_cast<const __nv_bfloat16*>(p.Z) + gm * p.ldz + n0 + c0;
+                                    unpack_bf16x8(*reinterpret_cast<const uint4*>(zr + 8 * v), z);
+                                }
 #pragma unroll
                                 for (int e = 0; e < 8; ++e)
                                     acc = fmaf(__uint_as_float(u[8 * v + e]), z[e], acc);
@@ -569,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld_32x32b_x32(trow + c0, u);
                 tmem_ld_wait();
                 if (gm < p.M) {
-                    const __nv_bfloat16* zr = p.Z + gm * p.ldz + n0 + c0;
+                    const __nv_bfloat16* zr = static_cast<const __nv_bfloat16*>(p.Z) + gm * p.ldz + n0 + c0;
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
                         if (c0 + 8 * v < bn_pair && n0 + c0 + 8 * v < p.N) {
@@ -647,29 +707,32 @@ __global__ void __launch_bounds__(256) gram_split(const float* __restrict__ g, i
     g2[i * 2 * r_pad + r_pad + j] = __float2bfloat16_rn(__fsub_rn(v, __bfloat162float(hi)));
 }
 
-int stages_for(int bn) {
-    const int stage = kXStage + bn * kBK * 2;
+int stages_for(int bn, bool f32 = false) {
+    const int stage = (kXStage + bn * kBK * 2) * (f32 ? 2 : 1);
     const int avail = kMaxSmem - 1024 - 256;
     return std::min(8, avail / stage);
 }
 
-size_t smem_for(int bn, int stages) {
-    return size_t(stages) * (kXStage + bn * kBK * 2) + 1024 + 256;
+size_t smem_for(int bn, int stages, bool f32 = false) {
+    return size_t(stages) * (kXStage + bn * kBK * 2) * (f32 ? 2 : 1) + 1024 + 256;
 }
 
 // tpc_pairs: launch as clusters of 2 so the kernel occupies whole TPCs (used for the
 // side-stream GEMMs that run beside the 2-SM W.A^T kernel, whose CTA pairs each need
 // a whole TPC; a lone side CTA per TPC would strand its sibling SM).
 cudaError_t launch_tc(int mode, const CUtensorMap& tx, const CUtensorMap& ty, TcParams p,
-                      dim3 grid, cudaStream_t st, const char* name, bool tpc_pairs = false) {
-    static bool attr[2] = {false, false};
-    const size_t smem = smem_for(p.bn, p.stages);
+                      dim3 grid, cudaStream_t st, const char* name, bool tpc_pairs = false,
+                      bool f32 = false) {
+    static bool attr[4] = {false, false, false, false};
+    const size_t smem = smem_for(p.bn, p.stages, f32);
     cudaError_t e;
-    auto kern = mode == kTcRowdot ? tc_rowdot<kTcRowdot> : tc_rowdot<kTcStore>;
-    if (!attr[mode]) {
+    auto kern = f32 ? (mode == kTcRowdot ? tc_rowdot<kTcRowdot, true> : tc_rowdot<kTcStore, true>)
+                    : (mode == kTcRowdot ? tc_rowdot<kTcRowdot> : tc_rowdot<kTcStore>);
+    const int ai = mode + (f32 ? 2 : 0);
+    if (!attr[ai]) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
         if (e != cudaSuccess) return e;
-        attr[mode] = true;
+        attr[ai] = true;
     }
     if (tpc_pairs) grid.x = (grid.x + 1) / 2 * 2;
     cudaLaunchConfig_t cfg = {};
@@ -1067,6 +1130,115 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
     f.m = a.m; f.mag_dt = a.mag_dt; f.g = a.m ? a.g : nullptr;
     if (partial) { f.w_norm = nullptr; f.g = nullptr; f.ba_sq = nullptr; }
     if (launches) ++*launches;
+    return launch_finish(f, st);
+}
+
+// fp32 weights (the accuracy configuration, BASELINE configs[0]): the same three GEMMs on
+// the tensor cores with 3xTF32 operands (tc_rowdot<., true>), serially on all SMs:
+// G = A A^T (split-K partial tiles, fixed-order reduction to fp32 G), U = W A^T with the
+// bitwise fp32 base_sq chain, V = B G (K = r), then the finisher.
+bool norm_tf32_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DFX_NORM_TF32");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+bool norm_tc_f32_supported(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk) {
+    return d_in >= 32 && d_in % 4 == 0 && r % 8 == 0 && r >= 16 && r <= 2048 && chunk % 32 == 0 &&
+           d_out >= 1 && d_in < (int64_t(1) << 31) && d_out < (int64_t(1) << 31);
+}
+
+cudaError_t launch_norm_tc_f32(const NormArgs& a, Workspace* ws, cudaStream_t st, int* launches) {
+    cudaError_t err = cudaSuccess;
+    constexpr int64_t kKB = 32;                       // fp32 elements per K block (128 bytes)
+    const int64_t r = a.r, d_out = a.d_out, d_in = a.d_in;
+    const int64_t m_tiles = (d_out + kBM - 1) / kBM;
+    const int64_t kb_in = (d_in + kKB - 1) / kKB;
+    const int64_t chunk_blocks = a.chunk_size / kKB;
+    const int64_t n_chunks = (d_in + a.chunk_size - 1) / a.chunk_size;
+    const int sms = ws_sm_count(ws);
+    const int nt = static_cast<int>((r + kBM - 1) / kBM);
+    const int gtiles = nt * (nt + 1) / 2;
+
+    // U: N / K splits as for bf16 (K splits only on ChunkPlan boundaries)
+    const Split sp = choose_split(m_tiles, r, kb_in, static_cast<int>(std::min<int64_t>(n_chunks, 8)), sms);
+    const int64_t kbps = (n_chunks + sp.ks - 1) / sp.ks * chunk_blocks;
+    const int uks = static_cast<int>((kb_in + kbps - 1) / kbps);
+    // G: split-K over the SMs
+    int gks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sms / gtiles, kb_in / 8)));
+    const int64_t gkbps = (kb_in + gks - 1) / gks;
+    gks = static_cast<int>((kb_in + gkbps - 1) / gkbps);
+    // V = B G: K = r
+    const int64_t kb_r = (r + kKB - 1) / kKB;
+    const Split sb = choose_split(m_tiles, r, kb_r, 1, sms);
+
+    float* cross = static_cast<float*>(ws_get(ws, kWsCross, size_t(uks) * sp.ns * d_out * 4, &err));
+    if (err != cudaSuccess) return err;
+    float* base = static_cast<float*>(ws_get(ws, kWsBase, size_t(n_chunks) * d_out * 4, &err));
+    if (err != cudaSuccess) return err;
+    float* gpart = static_cast<float*>(ws_get(ws, kWsGramPart, size_t(gks) * gtiles * kBM * kBM * 4, &err));
+    if (err != cudaSuccess) return err;
+    float* G = static_cast<float*>(ws_get(ws, kWsGram, size_t(r) * r * 4, &err));
+    if (err != cudaSuccess) return err;
+    float* ba = static_cast<float*>(ws_get(ws, kWsBa, size_t(sb.ns) * d_out * 4, &err));
+    if (err != cudaSuccess) return err;
+
+    // G = A A^T -> fixed-order split sum, mirrored, fp32
+    {
+        CUtensorMap ta;
+        if ((err = make_tmap_2d(&ta, kF32, a.a, r, d_in, d_in * 4, kKB, kBM, true)) != cudaSuccess) return err;
+        TcParams p{};
+        p.M = r; p.N = r; p.k_total = d_in; p.kb_per_split = static_cast<int>(gkbps); p.n_split = 1;
+        p.bn = kBM; p.stages = stages_for(kBM, true); p.chunk = a.chunk_size;
+        p.out = gpart; p.gram_nt = nt; p.tiles = gtiles;
+        const int gx = std::min(gtiles, std::max(1, sms / gks));
+        if ((err = launch_tc(kTcStore, ta, ta, p, dim3(gx, gks), st, "gram_tf32x3", false, true)) != cudaSuccess)
+            return err;
+        prof_begin("gram_reduce", st);
+        gram_reduce<<<static_cast<unsigned>((r * r + 255) / 256), 256, 0, st>>>(gpart, gks, nt, r, r,
+                                                                                 nullptr, G);
+        prof_end(st);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    }
+    // U = W A^T, cross = rowdot(U, B), base_sq chain
+    {
+        CUtensorMap tw, ta;
+        if ((err = make_tmap_2d(&tw, kF32, a.w, d_out, d_in, d_in * 4, kKB, kBM, true)) != cudaSuccess) return err;
+        if ((err = make_tmap_2d(&ta, kF32, a.a, r, d_in, d_in * 4, kKB, sp.bn, true)) != cudaSuccess) return err;
+        TcParams p{};
+        p.M = d_out; p.N = r; p.k_total = d_in; p.kb_per_split = static_cast<int>(kbps);
+        p.n_split = sp.ns; p.bn = sp.bn; p.stages = stages_for(sp.bn, true); p.chunk = a.chunk_size;
+        p.Z = a.b; p.ldz = r; p.out = cross; p.base_out = base; p.do_chain = 1;
+        p.tiles = static_cast<int>(m_tiles * sp.ns);
+        const int gx = std::min<int>(p.tiles, std::max(1, sms / uks));
+        if ((err = launch_tc(kTcRowdot, tw, ta, p, dim3(gx, uks), st, "u_rowdot_tf32x3", false, true)) != cudaSuccess)
+            return err;
+    }
+    // V = B G, ba_sq = rowdot(V, B)
+    {
+        CUtensorMap tb, tg;
+        if ((err = make_tmap_2d(&tb, kF32, a.b, d_out, r, r * 4, kKB, kBM, true)) != cudaSuccess) return err;
+        if ((err = make_tmap_2d(&tg, kF32, G, r, r, r * 4, kKB, sb.bn, true)) != cudaSuccess) return err;
+        TcParams p{};
+        p.M = d_out; p.N = r; p.k_total = r; p.kb_per_split = static_cast<int>(kb_r);
+        p.n_split = sb.ns; p.bn = sb.bn; p.stages = stages_for(sb.bn, true); p.chunk = a.chunk_size;
+        p.Z = a.b; p.ldz = r; p.out = ba; p.do_chain = 0;
+        p.tiles = static_cast<int>(m_tiles * sb.ns);
+        if ((err = launch_tc(kTcRowdot, tb, tg, p, dim3(std::min(p.tiles, sms), 1), st, "ba_rowdot_tf32x3",
+                             false, true)) != cudaSuccess)
+            return err;
+    }
+    if (launches) *launches += 5;
+    FinishArgs f{};
+    f.base_part = base; f.base_parts = static_cast<int>(n_chunks);
+    f.cross_part = cross; f.cross_parts = uks * sp.ns;
+    f.ba_part = ba; f.ba_parts = sb.ns;
+    f.d_out = d_out; f.two_s = 2.0 * a.s; f.s2 = a.s * a.s;
+    f.base_sq = a.base_sq; f.cross = a.cross; f.ba_sq = a.ba_sq;
+    f.round_dt = a.round_dt; f.w_norm = a.w_norm;
+    f.m = a.m; f.mag_dt = a.mag_dt; f.g = a.m ? a.g : nullptr;
     return launch_finish(f, st);
 }
 

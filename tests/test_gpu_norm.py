@@ -277,3 +277,48 @@ def test_sm_budget_full_size_c2(oracle):
     assert np.all(np.abs(t[1][rows] - sub[1]) <= 2e-5 * np.sqrt(sub[0] * sub[2]))
     assert np.all(np.abs(t[2][rows] - sub[2]) <= 1e-4 * sub[2])
     dfx.close()
+
+
+@pytest.mark.parametrize("d_out,d_in,r,cs", [(256, 512, 64, None), (1024, 1024, 384, None),
+                                             (300, 640, 40, None), (136, 2048, 512, None),
+                                             (512, 1024, 128, 256), (384, 4096, 96, 1536)])
+def test_fp32_tensor_core_path(dfx, oracle, d_out, d_in, r, cs):
+    """fp32 weights on tcgen05 (3xTF32, fp32-class accumulation): base_sq bitwise (serial
+    chain, chunk partials), cross / ba_sq within the fp32 bounds of the oracle's terms, the
+    norm within max(1e-5, 64 kappa 2^-24) of fp64 — the reference's own bar."""
+    assert dfx.uses_tensor_cores(0, d_out, d_in, r)
+    W, A, B = _fixture(oracle, d_out, d_in, r, 7 * d_out + r, dt=0)
+    s = 2.0 / np.sqrt(r)
+    if cs is None:
+        cs, _ = oracle.plan_chunks(d_out, d_in)
+    want = oracle.norm_terms(W, A, B, s, cs)
+    m = np.abs(oracle.gaussian_vector(d_out, 1.0, 0.1, 5))
+    wn, g, t = _row_norm(dfx, W, A, B, s, cs, 0, m=m)
+    assert bits_equal(t[0], want[0])
+    scale_c = np.sqrt(want[0] * np.abs(want[2])) + 1e-30
+    assert np.all(np.abs(t[1] - want[1]) <= 2e-5 * scale_c + 1e-6 * np.abs(want[1]))
+    assert np.all(np.abs(t[2] - want[2]) <= 1e-4 * np.abs(want[2]) + 1e-6 * want[2].max())
+    f64 = oracle.dense_row_norm_f64(W, A, B, s)
+    kappa = _kappa(oracle, W, A, B, s)
+    assert np.all(np.abs(wn - f64) <= np.maximum(1e-5, 64 * kappa * 2.0 ** -24) * f64)
+    assert bits_equal(g, oracle.magnitude_scale(0, m, wn))
+
+
+def test_fp32_c1_full_size(dfx, oracle):
+    """BASELINE C1 (4096^2, r = 384, fp32) at full size on the 3xTF32 path: base_sq bitwise
+    on every row, sampled rows' norms vs fp64 within the reference's bar."""
+    d_out = d_in = 4096
+    r = 384
+    rng = np.random.default_rng(4)
+    W = rng.standard_normal((d_out, d_in), dtype=np.float32)
+    A = rng.standard_normal((r, d_in), dtype=np.float32)
+    B = rng.standard_normal((d_out, r), dtype=np.float32)
+    s = 2.0 / np.sqrt(r)
+    cs, _ = oracle.plan_chunks(d_out, d_in)
+    wn, _, t = _row_norm(dfx, W, A, B, s, cs, 0)
+    assert bits_equal(t[0], oracle.norm_terms(W, A, B, 0.0, cs)[0])
+    rows = np.sort(rng.choice(d_out, 64, replace=False))
+    Ws, Bs = np.ascontiguousarray(W[rows]), np.ascontiguousarray(B[rows])
+    f64 = oracle.dense_row_norm_f64(Ws, A, Bs, s)
+    kappa = _kappa(oracle, Ws, A, Bs, s)
+    assert np.all(np.abs(wn[rows] - f64) <= np.maximum(1e-5, 64 * kappa * 2.0 ** -24) * f64)

@@ -1163,7 +1163,17 @@ cudaError_t launch_norm_tc_f32(const NormArgs& a, Workspace* ws, cudaStream_t st
     const int gtiles = nt * (nt + 1) / 2;
 
     // U: N / K splits as for bf16 (K splits only on ChunkPlan boundaries)
-    const Split sp = choose_split(m_tiles, r, kb_in, static_cast<int>(std::min<int64_t>(n_chunks, 8)), sms);
+    Split sp = choose_split(m_tiles, r, kb_in, static_cast<int>(std::min<int64_t>(n_chunks, 8)), sms);
+    {
+        // 3xTF32 issues the same 12 UMMAs per K block whatever N is, and its stage holds the
+        // low parts too: use as many N splits as fill the SMs (smaller stages, more of them;
+        // measured at C1: N = 96 x 4 splits 230 us vs N = 192 x 2 313 us)
+        const int ns_min = static_cast<int>((r + 255) / 256);
+        const int ns = static_cast<int>(std::max<int64_t>(
+            ns_min, std::min<int64_t>(std::max<int64_t>(1, sms / std::max<int64_t>(1, m_tiles * sp.ks)),
+                                      std::max<int64_t>(1, r / 32))));
+        sp = {ns, sp.ks, static_cast<int>(((r + ns - 1) / ns + 15) / 16 * 16)};
+    }
     const int64_t kbps = (n_chunks + sp.ks - 1) / sp.ks * chunk_blocks;
     const int uks = static_cast<int>((kb_in + kbps - 1) / kbps);
     // G: split-K over the SMs

@@ -1,10 +1,7 @@
 #!/bin/bash
 O=gpurun_out/exp.txt; : > $O
-B="timeout 120 python bench.py --no-cpu-baseline --e2e-steps 0 --lora-steps 0 --variant-steps 0 --steps 2000"
-run() { echo "== $*" >> $O; $B "$@" 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'])" >> $O 2>&1; }
-run --pipeline 8
-run --pipeline 16
-run --pipeline 40
-run --pipeline 40 --nbuf 8
-run --pipeline 16 --mode infer
-run --pipeline 40 --mode infer
+B="timeout 120 python bench.py --config c1 --mode infer --steps 200 --e2e-steps 0 --lora-steps 0 --variant-steps 0 --no-cpu-baseline"
+for ns in 0 2 3 4 6; do
+  echo "== ns $ns" >> $O
+  if [ $ns = 0 ]; then $B 2>/dev/null; else DFX_F32_NS=$ns $B 2>/dev/null; fi | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], {k:v['avg_us'] for k,v in d['kernels'].items()})" >> $O 2>&1
+done

@@ -20,7 +20,7 @@ __all__ = ["Dfx", "build", "LIB_PATH", "DROPIN_PATH", "F32", "BF16", "F16", "Dfx
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 ROOT_DIR = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "libdfx.so")
+LIB_PATH = os.environ.get("DFX_LIB", os.path.join(PKG_DIR, "libdfx.so"))   # DFX_LIB: A/B builds
 DROPIN_PATH = os.path.join(PKG_DIR, "libdorafactor_b200.so")
 HEADER_PATH = os.path.join(ROOT_DIR, "include", "dfx.h")
 

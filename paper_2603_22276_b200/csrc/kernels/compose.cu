@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "launch.h"
 #include "ptx.cuh"
@@ -132,9 +133,25 @@ __global__ void __launch_bounds__(256) compose_fwd_vec(const T* __restrict__ bas
                                                        const float* __restrict__ g, float sf,
                                                        int64_t rows, int64_t d_out,
                                                        T* __restrict__ delta,
-                                                       T* __restrict__ inner) {
+                                                       T* __restrict__ inner, int pf_rows) {
     constexpr int V = Vec<T>::N;
     const int64_t cv = d_out / V;
+    // L2 prefetch of the block `pf_rows` rows ahead (about one wave of resident CTAs), so
+    // the loads of the CTAs that follow this one hit L2: bytes in flight per SM are capped
+    // by the registers of the ~2 resident CTAs, L2 latency is far below HBM's
+    if (pf_rows > 0 && threadIdx.x == 0 && threadIdx.y == 0) {
+        const int64_t c0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
+        const int64_t nvec = min(int64_t(blockDim.x), cv - c0);
+        const uint32_t bytes = static_cast<uint32_t>(nvec * 16);
+        const int64_t rp0 = static_cast<int64_t>(blockIdx.y) * blockDim.y * R + pf_rows;
+        for (int i = 0; i < blockDim.y * R; ++i) {
+            const int64_t rr = rp0 + i;
+            if (rr >= rows) break;
+            const int64_t off = rr * d_out + c0 * V;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + off), "r"(bytes) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lora + off), "r"(bytes) : "memory");
+        }
+    }
     const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (c >= cv) return;
     float gv[V], gm1[V];
@@ -441,10 +458,16 @@ cudaError_t fwd_impl(const void* base, const void* lora, const float* g, float s
         const int by = 256 / bx;
         const int64_t gx = (cv + bx - 1) / bx;
         const int64_t gy = std::min<int64_t>((rows + by * R - 1) / (by * R), 65535);
+        // prefetch distance: one wave of resident CTAs (2 per SM at this register count);
+        // measured at C2: dual 45.8 -> 43.3 us, 71 -> 61 us on a 76-SM partition
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int pf_rows = static_cast<int>(2 * sms / gx) * by * R;
         prof_begin(kInner ? "compose_fwd_dual" : "compose_fwd", st);
         compose_fwd_vec<T, kInner, R>
             <<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)), dim3(bx, by), 0, st>>>(
-                b, l, g, sf, rows, d_out, d, in);
+                b, l, g, sf, rows, d_out, d, in, pf_rows);
         prof_end(st);
     } else {
         const int64_t n = rows * d_out;

@@ -1,7 +1,9 @@
 #!/bin/bash
 O=gpurun_out/exp.txt; : > $O
-B="timeout 120 python bench.py --config c1 --mode infer --steps 200 --e2e-steps 0 --lora-steps 0 --variant-steps 0 --no-cpu-baseline"
-for ns in 0 2 3 4 6; do
-  echo "== ns $ns" >> $O
-  if [ $ns = 0 ]; then $B 2>/dev/null; else DFX_F32_NS=$ns $B 2>/dev/null; fi | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], {k:v['avg_us'] for k,v in d['kernels'].items()})" >> $O 2>&1
+for st in 4 8 10 12; do
+  echo "== bwd stages $st" >> $O
+  DFX_LIB=variants/libdfx_bwd$st.so timeout 60 python scripts/exp_kernels.py --what bwd --tag st$st >> $O 2>&1
+  DFX_LIB=variants/libdfx_bwd$st.so timeout 120 python scripts/exp_green.py 72 80 bwd 2>&1 | tail -1 >> $O
+  DFX_LIB=variants/libdfx_bwd$st.so timeout 120 python bench.py --no-cpu-baseline --e2e-steps 0 --lora-steps 0 --variant-steps 0 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('bench', d['value'], d['ms_per_step'])" >> $O 2>&1
 done
+timeout 60 python scripts/exp_kernels.py --what bwd,dual --tag st6 >> $O 2>&1

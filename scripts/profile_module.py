@@ -25,7 +25,7 @@ def main():
     dfx = P.Dfx(0)
     dfx.set_sm_budget(a.budget)
     cs, _ = P.plan_chunks(d_out, d_in)
-    bf = torch.bfloat16
+    bf = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[cfg["dtype"]]
     W = torch.randn(d_out, d_in, device="cuda").to(bf)
     A = torch.randn(r, d_in, device="cuda").to(bf)
     B = torch.randn(d_out, r, device="cuda").to(bf)

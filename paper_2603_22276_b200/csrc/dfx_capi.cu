@@ -107,6 +107,20 @@ EncodeFn encode_fn() {
 }
 }  // namespace
 
+cudaError_t ensure_max_dyn_smem(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void*, int>, int>> done;   // (func, dev) -> bytes
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& d : done)
+        if (d.first.first == func && d.first.second == dev && d.second >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.push_back({{func, dev}, bytes});
+    return e;
+}
+
 cudaError_t make_tmap_2d(CUtensorMap* out, int dt, const void* base, uint64_t rows, uint64_t cols,
                          uint64_t row_pitch_bytes, uint32_t box_cols, uint32_t box_rows,
                          bool swizzle128) {

@@ -521,13 +521,8 @@ cudaError_t bwd_impl(int dt, const void* dy, const float* g, float sf, const voi
         if (e != cudaSuccess) return e;
         e = make_tmap_2d(&tm_in, dt, inner, rows, d_out, pitch, C::kSC, C::kRB, false);
         if (e != cudaSuccess) return e;
-        static bool attr_set = false;
-        if (!attr_set) {
-            e = cudaFuncSetAttribute(compose_bwd_serial<T>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-            if (e != cudaSuccess) return e;
-            attr_set = true;
-        }
+        e = ensure_max_dyn_smem(reinterpret_cast<const void*>(compose_bwd_serial<T>), C::kSmem);
+        if (e != cudaSuccess) return e;
         const unsigned grid = static_cast<unsigned>((d_out + C::kSC - 1) / C::kSC);
         prof_begin("compose_bwd_dmag", st);
         compose_bwd_serial<T><<<grid, C::kThreads, C::kSmem, st>>>(

@@ -23,6 +23,10 @@ cudaError_t make_tmap_2d_sw(CUtensorMap* out, int dt, const void* base, uint64_t
                             uint64_t cols, uint64_t row_pitch_bytes, uint32_t box_cols,
                             uint32_t box_rows, int swizzle_bytes);
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `func` on the current device, set once per
+// (function, device) pair (thread-safe; a process may drive several devices).
+cudaError_t ensure_max_dyn_smem(const void* func, int bytes);
+
 // ---------------------------------------------------------------- compose
 cudaError_t launch_compose_fwd(int dt, const void* base, const void* lora, const float* g, float sf,
                                int64_t rows, int64_t d_out, void* delta, void* inner,

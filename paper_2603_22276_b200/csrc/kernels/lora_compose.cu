@@ -388,8 +388,7 @@ cudaError_t launch_lora_compose(int dt, const void* mid, const void* b, const vo
     p.base = base;
     p.fp16 = dt == kF16;
     const size_t smem = lc_smem(p.stages, p.n_out);
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+    e = ensure_max_dyn_smem(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const int grid = std::min(p.tiles, sms);
     prof_begin("lora_compose_tc", st);

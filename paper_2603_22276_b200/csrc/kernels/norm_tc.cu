@@ -723,17 +723,11 @@ size_t smem_for(int bn, int stages, bool f32 = false) {
 cudaError_t launch_tc(int mode, const CUtensorMap& tx, const CUtensorMap& ty, TcParams p,
                       dim3 grid, cudaStream_t st, const char* name, bool tpc_pairs = false,
                       bool f32 = false) {
-    static bool attr[4] = {false, false, false, false};
     const size_t smem = smem_for(p.bn, p.stages, f32);
     cudaError_t e;
     auto kern = f32 ? (mode == kTcRowdot ? tc_rowdot<kTcRowdot, true> : tc_rowdot<kTcStore, true>)
                     : (mode == kTcRowdot ? tc_rowdot<kTcRowdot> : tc_rowdot<kTcStore>);
-    const int ai = mode + (f32 ? 2 : 0);
-    if (!attr[ai]) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-        if (e != cudaSuccess) return e;
-        attr[ai] = true;
-    }
+    if ((e = ensure_max_dyn_smem(reinterpret_cast<const void*>(kern), kMaxSmem)) != cudaSuccess) return e;
     if (tpc_pairs) grid.x = (grid.x + 1) / 2 * 2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -765,14 +759,9 @@ int stages_for_pair(int bn, int nh = 1) {
 
 cudaError_t launch_tc_pair(const CUtensorMap& tx, const CUtensorMap& ty, TcParams p, int pairs,
                            int ks, cudaStream_t st, const char* name) {
-    static bool attr = false;
     cudaError_t e;
-    if (!attr) {
-        e = cudaFuncSetAttribute(tc_pair_rowdot, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kMaxSmem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if ((e = ensure_max_dyn_smem(reinterpret_cast<const void*>(tc_pair_rowdot), kMaxSmem)) != cudaSuccess)
+        return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs, ks, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);

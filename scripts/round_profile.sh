@@ -17,5 +17,5 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:lora
     -o gpurun_out/${R}_ncu_lora_compose python scripts/exp_kernels.py --what lora_fused --iters 1 > /dev/null 2>&1
 ls gpurun_out | grep $R
 # fp32 weights on the tensor cores (3xTF32, BASELINE configs[0])
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:tc_rowdot -s 2 -c 1 \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:tc_rowdot -s 1 -c 1 \
     -o gpurun_out/${R}_ncu_tc_rowdot_tf32x3_c1 python scripts/profile_module.py --config c1 --steps 2 > /dev/null 2>&1

@@ -329,16 +329,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
             for (int it = 0; it < nkb; ++it) {
                 mbar_wait(&full[s], ph);
-                const uint4* src = reinterpret_cast<const uint4*>(smem + s * stage_bytes);
-                uint4* dst = reinterpret_cast<uint4*>(smem + s * stage_bytes + raw_bytes);
+                const uint32_t src = smem_u32(smem + s * stage_bytes);
+                const uint32_t dst = src + static_cast<uint32_t>(raw_bytes);
+#pragma unroll 4
                 for (int i = st; i < raw_bytes / 16; i += 64) {
-                    const uint4 w = src[i];
-                    uint4 l;
-                    l.x = __float_as_uint(__fsub_rn(__uint_as_float(w.x), __uint_as_float(w.x & 0xFFFFE000u)));
-                    l.y = __float_as_uint(__fsub_rn(__uint_as_float(w.y), __uint_as_float(w.y & 0xFFFFE000u)));
-                    l.z = __float_as_uint(__fsub_rn(__uint_as_float(w.z), __uint_as_float(w.z & 0xFFFFE000u)));
-                    l.w = __float_as_uint(__fsub_rn(__uint_as_float(w.w), __uint_as_float(w.w & 0xFFFFE000u)));
-                    dst[i] = l;
+                    uint32_t w[4];
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                                 : "r"(src + i * 16));
+                    uint32_t l[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        l[e] = __float_as_uint(__fsub_rn(__uint_as_float(w[e]),
+                                                         __uint_as_float(w[e] & 0xFFFFE000u)));
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst + i * 16),
+                                 "r"(l[0]), "r"(l[1]), "r"(l[2]), "r"(l[3])
+                                 : "memory");
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();

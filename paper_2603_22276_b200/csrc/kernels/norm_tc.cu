@@ -189,8 +189,10 @@ __device__ __forceinline__ void tile_coords(int kMode, const TcParams& p, int t,
 // tiles, and every K=8 step issues three kind::tf32 UMMAs, X.Y + X.Y_lo + X_lo.Y (the raw
 // fp32 operand is read as its TF32 truncation), which carries ~2^-21 relative error —
 // fp32-class accumulation on the tensor cores.
+constexpr int kSplitWarps = 4;                   // 3xTF32: warps 6 .. 6 + kSplitWarps - 1
+
 template <int kMode, bool kF32 = false>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kF32 ? kThreads + 32 * (kSplitWarps - 2) : kThreads, 1)
     tc_rowdot(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
               const TcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tmem_full[a], 1);
             mbar_init(&tmem_empty[a], 4);
         }
-        for (int s = 0; s < p.stages; ++s) mbar_init(&split[s], 2);
+        for (int s = 0; s < p.stages; ++s) mbar_init(&split[s], kSplitWarps);
         fence_mbar_init();
     }
     if (warp == kWarpMma) {
@@ -323,7 +325,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (kF32 && nkb > 0 && warp >= 6) {
         // ================= 3xTF32 split: low parts x - tf32(x) of both tiles ==========
-        const int st = (warp - 6) * 32 + lane;                  // 0 .. 63
+        const int st = (warp - 6) * 32 + lane;                  // 0 .. 32 * kSplitWarps - 1
+        constexpr int kST = 32 * kSplitWarps;
         int s = 0;
         uint32_t ph = 0;
         for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
@@ -331,20 +334,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&full[s], ph);
                 const uint32_t src = smem_u32(smem + s * stage_bytes);
                 const uint32_t dst = src + static_cast<uint32_t>(raw_bytes);
-#pragma unroll 4
-                for (int i = st; i < raw_bytes / 16; i += 64) {
-                    uint32_t w[4];
-                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
-                                 : "r"(src + i * 16));
-                    uint32_t l[4];
+                // batches of 8 16-byte words per thread: all loads first, then the stores
+                const int n16 = raw_bytes / 16;
+                for (int i0 = st; i0 < n16; i0 += kST * 8) {
+                    uint32_t w[8][4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        l[e] = __float_as_uint(__fsub_rn(__uint_as_float(w[e]),
-                                                         __uint_as_float(w[e] & 0xFFFFE000u)));
-                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst + i * 16),
-                                 "r"(l[0]), "r"(l[1]), "r"(l[2]), "r"(l[3])
-                                 : "memory");
+                    for (int b = 0; b < 8; ++b) {
+                        const int i = i0 + kST * b;
+                        if (i < n16)
+                            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(w[b][0]), "=r"(w[b][1]), "=r"(w[b][2]), "=r"(w[b][3])
+                                         : "r"(src + i * 16));
+                    }
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        const int i = i0 + kST * b;
+                        if (i >= n16) break;
+                        uint32_t l[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            l[e] = __float_as_uint(__fsub_rn(__uint_as_float(w[b][e]),
+                                                             __uint_as_float(w[b][e] & 0xFFFFE000u)));
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst + i * 16),
+                                     "r"(l[0]), "r"(l[1]), "r"(l[2]), "r"(l[3])
+                                     : "memory");
+                    }
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
@@ -737,7 +751,7 @@ cudaError_t launch_tc(int mode, const CUtensorMap& tx, const CUtensorMap& ty, Tc
     if (tpc_pairs) grid.x = (grid.x + 1) / 2 * 2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.blockDim = dim3(f32 ? kThreads + 32 * (kSplitWarps - 2) : kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];

@@ -333,6 +333,12 @@ def run_gpu(args, rank, world, local_rank, dist):
 
     def timed(mode, steps, warmup, clocks=None):
         set_budget(mode)
+        # one eager pass under this plan first: the context grows its workspace outside of
+        # graph capture (allocation is not capturable)
+        with torch.cuda.stream(stream):
+            for b in sets:
+                step(b, mode)
+        torch.cuda.synchronize()
         graphs, npipe = build_graphs(mode)
         nrep = len(graphs)
         with torch.cuda.stream(stream):

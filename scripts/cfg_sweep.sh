@@ -1,6 +1,6 @@
 #!/bin/bash
 # value + per-kernel times for each config (analysis helper); extra args go to bench.py
-O=gpurun_out/sweep.txt; : > $O
+O=${SWEEP_OUT:-gpurun_out/sweep.txt}; : > $O
 for cfg in c2 c3 c4r64 c4r128 c4r512 c4r1024 c1; do
   for mode in train infer; do
     timeout 300 python bench.py --config $cfg --mode $mode --steps 400 --e2e-steps 0 --lora-steps 0 --variant-steps 0 --no-cpu-baseline "$@" > /tmp/c.json 2>/tmp/c.err || { echo "$cfg $mode failed" >> $O; tail -3 /tmp/c.err >> $O; continue; }

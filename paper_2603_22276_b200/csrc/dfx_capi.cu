@@ -584,6 +584,12 @@ int dfx_lora_compose(dfx_ctx* ctx, dfx_dtype dtype, const void* mid, const void*
         return fail(DFX_EINVAL, "lora_compose: null operand");
     if ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(bias)) & 15u)
         return fail(DFX_EINVAL, "lora_compose: g and bias must be 16-byte aligned");
+    const uintptr_t tiles = reinterpret_cast<uintptr_t>(mid) | reinterpret_cast<uintptr_t>(B) |
+                            reinterpret_cast<uintptr_t>(base) | reinterpret_cast<uintptr_t>(y) |
+                            reinterpret_cast<uintptr_t>(delta) | reinterpret_cast<uintptr_t>(inner) |
+                            reinterpret_cast<uintptr_t>(lora);
+    if (tiles & 15u)
+        return fail(DFX_EINVAL, "lora_compose: matrices must be 16-byte aligned (TMA / 128-bit access)");
     int launches = 0;
     const cudaError_t e = dfx::launch_lora_compose(dtype, mid, B, base, g, static_cast<float>(s),
                                                    bias, rows, d_out, r, y, delta, inner, lora,

@@ -147,3 +147,12 @@ def test_lora_compose_rejects(dfx):
     b = torch.zeros(4, 8, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(P.DfxError):
         dfx.lora_compose(b, b, b, g, 1.0, y=b, delta=b, inner=b, lora=b)   # > 3 outputs
+    B8 = torch.zeros(8, 8, device="cuda", dtype=torch.bfloat16)        # d_out = r = 8: valid
+    dfx.lora_compose(b, B8, b, g, 1.0, y=torch.empty_like(b))
+    flat = torch.zeros(4 * 8 + 1, device="cuda", dtype=torch.bfloat16)
+    mis = flat[1:].view(4, 8)                                           # 2-byte offset
+    with pytest.raises(P.DfxInvalidArgument):
+        dfx.lora_compose(b, B8, mis, g, 1.0, y=torch.empty_like(b))
+    g12 = torch.ones(12, device="cuda")
+    with pytest.raises(P.DfxInvalidArgument):
+        dfx.lora_compose(b, B8, b, g12[1:9], 1.0, y=torch.empty_like(b))  # misaligned g

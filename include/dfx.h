@@ -137,7 +137,9 @@ int dfx_compose_fwd(dfx_ctx* ctx, dfx_dtype dtype, const void* base, const void*
 
 /* compose_backward (compose.hpp:73-75): d_lora = g*s*dY, d_base = (g-1)*dY; when
  * d_mag != NULL (mag_grad) also d_mag = serial-per-column sum(dY*inner) / w_norm,
- * bitwise equal to the reference's fixed serial order.  inner/w_norm required then. */
+ * bitwise equal to the reference's fixed serial order.  inner/w_norm required then.
+ * With d_mag != NULL, d_lora and d_base may both be NULL: magnitude gradient only (a caller
+ * that produced d_lora / d_base per row chunk with d_mag == NULL). */
 int dfx_compose_bwd(dfx_ctx* ctx, dfx_dtype dtype, const void* dy, const float* g, double s,
                     const void* inner, const float* w_norm, int64_t rows, int64_t d_out,
                     void* d_lora, void* d_base, float* d_mag, dfx_stream_t stream);

@@ -534,7 +534,9 @@ int dfx_compose_bwd(dfx_ctx* ctx, dfx_dtype dtype, const void* dy, const float* 
     if (d_mag && !inner && rows > 0)
         return fail(DFX_EINVAL, "compose_backward: magnitude gradient requires inner");
     if (d_mag && !w_norm) return fail(DFX_EINVAL, "compose_backward: w_norm length != d_out");
-    if (rows > 0 && d_out > 0 && (!dy || !g || !d_lora || !d_base))
+    // d_lora and d_base may both be null when d_mag is requested: magnitude gradient only
+    const bool mag_only = d_mag && !d_lora && !d_base;
+    if (rows > 0 && d_out > 0 && (!dy || !g || (!mag_only && (!d_lora || !d_base))))
         return fail(DFX_EINVAL, "compose_backward: null operand");
     int launches = 0;
     const cudaError_t e =
@@ -752,49 +754,50 @@ int dfx_module_train_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const vo
     cudaStreamWaitEvent(ctx->st_d2h, ev_norm, 0);
     cudaMemcpyAsync(g, dg, d_out * 4, cudaMemcpyDeviceToHost, ctx->st_d2h);
 
-    // forward in row chunks (upload c+1 while composing c and downloading c-1); the dual
-    // output's inner stays on the device for the magnitude gradient
+    // Row chunks: upload base / lora / dY of chunk c+1 while chunk c runs the dual compose and
+    // the elementwise backward (d_lora, d_base) and chunk c-1 downloads delta / d_lora /
+    // d_base; the serial d_mag chain needs every row, so it runs last over the resident dY
+    // and inner (magnitude-gradient-only backward) — PCIe stays busy in both directions.
     const int64_t nchunk = rows >= 1024 ? 8 : 1;
     const int64_t crow = rows > 0 ? (rows + nchunk - 1) / nchunk : 1;
     for (int64_t r0 = 0; r0 < rows; r0 += crow) {
         const int64_t nr = std::min(crow, rows - r0);
         const size_t off = size_t(r0) * d_out * eb, bytes = size_t(nr) * d_out * eb;
-        cudaMemcpyAsync(static_cast<char*>(dbase) + off, static_cast<const char*>(base) + off,
-                        bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
-        cudaMemcpyAsync(static_cast<char*>(dlora) + off, static_cast<const char*>(lora) + off,
-                        bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        auto at = [&](void* p) { return static_cast<char*>(p) + off; };
+        auto atc = [&](const void* p) { return static_cast<const char*>(p) + off; };
+        cudaMemcpyAsync(at(dbase), atc(base), bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        cudaMemcpyAsync(at(dlora), atc(lora), bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        cudaMemcpyAsync(at(ddy), atc(dy), bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
         cudaEvent_t ein = event();
         cudaEventRecord(ein, ctx->st_h2d);
         cudaStreamWaitEvent(ctx->st_comp, ein, 0);
         int launches = 0;
-        e = dfx::launch_compose_fwd(dtype, static_cast<char*>(dbase) + off,
-                                    static_cast<char*>(dlora) + off, dg, static_cast<float>(s), nr,
-                                    d_out, static_cast<char*>(ddelta) + off,
-                                    static_cast<char*>(dinner) + off, ctx->st_comp, &launches);
+        e = dfx::launch_compose_fwd(dtype, at(dbase), at(dlora), dg, static_cast<float>(s), nr,
+                                    d_out, at(ddelta), at(dinner), ctx->st_comp, &launches);
+        if (e == cudaSuccess)
+            e = dfx::launch_compose_bwd(dtype, at(ddy), dg, static_cast<float>(s), nullptr, nullptr,
+                                        nr, d_out, at(ddl), at(ddb), nullptr, ctx->st_comp,
+                                        &launches);
         ctx->launches += launches;
         if (e != cudaSuccess) return cuda_fail(e, "dfx_module_train_host/compose");
         cudaEvent_t eout = event();
         cudaEventRecord(eout, ctx->st_comp);
         cudaStreamWaitEvent(ctx->st_d2h, eout, 0);
-        cudaMemcpyAsync(static_cast<char*>(delta) + off, static_cast<char*>(ddelta) + off, bytes,
-                        cudaMemcpyDeviceToHost, ctx->st_d2h);
+        cudaMemcpyAsync(static_cast<char*>(delta) + off, at(ddelta), bytes, cudaMemcpyDeviceToHost,
+                        ctx->st_d2h);
+        cudaMemcpyAsync(static_cast<char*>(d_lora) + off, at(ddl), bytes, cudaMemcpyDeviceToHost,
+                        ctx->st_d2h);
+        cudaMemcpyAsync(static_cast<char*>(d_base) + off, at(ddb), bytes, cudaMemcpyDeviceToHost,
+                        ctx->st_d2h);
     }
-    // backward: dY streams up behind the forward's activations; the serial d_mag chain
-    // needs every row, so the backward runs once dY is resident
-    cudaMemcpyAsync(ddy, dy, nact * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
-    cudaEvent_t ev_dy = event();
-    cudaEventRecord(ev_dy, ctx->st_h2d);
-    cudaStreamWaitEvent(ctx->st_comp, ev_dy, 0);
     int launches = 0;
     e = dfx::launch_compose_bwd(dtype, ddy, dg, static_cast<float>(s), dinner, dwn, rows, d_out,
-                                ddl, ddb, ddm, ctx->st_comp, &launches);
+                                nullptr, nullptr, ddm, ctx->st_comp, &launches);
     ctx->launches += launches;
-    if (e != cudaSuccess) return cuda_fail(e, "dfx_module_train_host/backward");
+    if (e != cudaSuccess) return cuda_fail(e, "dfx_module_train_host/d_mag");
     cudaEvent_t ev_bwd = event();
     cudaEventRecord(ev_bwd, ctx->st_comp);
     cudaStreamWaitEvent(ctx->st_d2h, ev_bwd, 0);
-    cudaMemcpyAsync(d_lora, ddl, nact * eb, cudaMemcpyDeviceToHost, ctx->st_d2h);
-    cudaMemcpyAsync(d_base, ddb, nact * eb, cudaMemcpyDeviceToHost, ctx->st_d2h);
     cudaMemcpyAsync(d_mag, ddm, d_out * 4, cudaMemcpyDeviceToHost, ctx->st_d2h);
     e = cudaStreamSynchronize(ctx->st_d2h);
     for (cudaEvent_t ev : evs) cudaEventDestroy(ev);

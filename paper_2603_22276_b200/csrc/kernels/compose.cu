@@ -377,7 +377,8 @@ __global__ void __launch_bounds__(SerialCfg<T>::kThreads, 1)
         constexpr int kVecPerRow = 128 / 16;                    // 8
         const int cvec = t % kVecPerRow;
         const int64_t j0 = col0 + cvec * V;
-        const bool col_ok = j0 < d_out;                          // d_out % V == 0 here
+        // d_lora == d_base == null: magnitude gradient only (the warps still pace the ring)
+        const bool col_ok = j0 < d_out && d_lora != nullptr;     // d_out % V == 0 here
         float gv[V], gm1[V];
 #pragma unroll
         for (int k = 0; k < V; ++k) {
@@ -430,8 +431,10 @@ __global__ void __launch_bounds__(128) compose_bwd_generic(const T* __restrict__
     for (int64_t i = 0; i < rows; ++i) {
         const int64_t e = i * d_out + j;
         const float y = Elem<T>::to_f(dy[e]);
-        d_lora[e] = Elem<T>::from_f(__fmul_rn(gf, __fmul_rn(sf, y)));
-        d_base[e] = Elem<T>::from_f(__fmul_rn(gm1, y));
+        if (d_lora) {                       // null with kMag: magnitude gradient only
+            d_lora[e] = Elem<T>::from_f(__fmul_rn(gf, __fmul_rn(sf, y)));
+            d_base[e] = Elem<T>::from_f(__fmul_rn(gm1, y));
+        }
         if (kMag) acc = __fadd_rn(acc, __fmul_rn(y, Elem<T>::to_f(inner[e])));
     }
     if (kMag) d_mag[j] = __fdiv_rn(acc, __ldg(w_norm + j));

@@ -178,3 +178,59 @@ def test_invalid_arguments(dfx):
                         w_norm=g, d_mag=torch.empty(8, device="cuda"))
     with pytest.raises(P.DfxInvalidArgument):
         dfx.compose_fwd(y, y, None, 1.0, torch.empty_like(y))
+
+
+@pytest.mark.parametrize("rows,d_out,dt", [(300, 264, 1), (4096, 1024, 1), (77, 40, 0), (129, 200, 2)])
+def test_backward_magnitude_only(dfx, oracle, rows, d_out, dt):
+    """dfx_compose_bwd with d_lora = d_base = NULL: the magnitude gradient alone, bitwise the
+    reference's serial per-column chain (used after a row-chunked elementwise backward)."""
+    import torch
+    o = oracle
+    seed = o.derive_seed(909, rows + d_out)
+    dy = o.gaussian_fixture(rows, d_out, 0.0, 1.0, o.derive_seed(seed, 1), dt)
+    inner = o.gaussian_fixture(rows, d_out, 0.0, 1.0, o.derive_seed(seed, 2), dt)
+    g = _g(o, d_out, dt, o.derive_seed(seed, 3))
+    wn = np.abs(_g(o, d_out, dt, o.derive_seed(seed, 4), sd=0.2)) + 0.5
+    want = o.compose_bwd(dt, dy, g, 0.75, inner, wn, mag_grad=True)[2]
+    dm = torch.empty(d_out, device="cuda")
+    dfx.compose_bwd(to_dev(dy, dt), torch.from_numpy(g).cuda(), 0.75, None, None,
+                    inner=to_dev(inner, dt), w_norm=torch.from_numpy(wn.astype(np.float32)).cuda(),
+                    d_mag=dm)
+    torch.cuda.synchronize()
+    assert bits_equal(dm.cpu().numpy(), want)
+
+
+def test_module_train_host_matches_device_path(dfx, oracle):
+    """dfx_module_train_host (row-chunked H2D / compose / D2H, magnitude gradient last) returns
+    exactly what the device-resident calls return."""
+    import math
+    import torch
+    import paper_2603_22276_b200 as P
+    d_out, d_in, r, rows = 512, 1024, 64, 2048
+    s = 2.0 / math.sqrt(r)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(3)
+    bf = torch.bfloat16
+    rnd = lambda *sh: torch.randn(*sh, device="cuda", generator=gen).to(bf)
+    W, A, B, base, lora, dy = rnd(d_out, d_in), rnd(r, d_in), rnd(d_out, r), rnd(rows, d_out), \
+        rnd(rows, d_out), rnd(rows, d_out)
+    m = torch.rand(d_out, device="cuda", generator=gen) * 10 + 20
+    cs, _ = P.plan_chunks(d_out, d_in)
+    wn, g = torch.empty(d_out, device="cuda"), torch.empty(d_out, device="cuda")
+    dfx.row_norm(W, A, B, s, cs, wn, m=m, g=g)
+    delta, inner, dl, db = (torch.empty_like(base) for _ in range(4))
+    dm = torch.empty(d_out, device="cuda")
+    dfx.compose_fwd(base, lora, g, s, delta, inner)
+    dfx.compose_bwd(dy, g, s, dl, db, inner=inner, w_norm=wn, d_mag=dm)
+    torch.cuda.synchronize()
+    h = {k: v.cpu().pin_memory() for k, v in dict(W=W, A=A, B=B, m=m, base=base, lora=lora, dy=dy).items()}
+    out = {k: torch.empty_like(h["base"]).pin_memory() for k in ("delta", "dl", "db")}
+    hdm = torch.empty(d_out).pin_memory()
+    hg = torch.empty(d_out).pin_memory()
+    dfx.module_train_host(P.BF16, h["W"], h["A"], h["B"], h["m"], h["base"], h["lora"], h["dy"], s,
+                          d_out, d_in, r, rows, cs, out["delta"], out["dl"], out["db"], hdm, hg)
+    assert torch.equal(hg, g.cpu())
+    assert torch.equal(out["delta"], delta.cpu())
+    assert torch.equal(out["dl"], dl.cpu())
+    assert torch.equal(out["db"], db.cpu())
+    assert torch.equal(hdm, dm.cpu())

@@ -921,7 +921,16 @@ UPlan plan_u(int64_t d_out, int64_t r, int64_t kb_in, int64_t chunk_blocks, int6
         const double c1 = gemm_cycles(pm_tiles * u.ks, pairs, kbps1, static_cast<int>(bnh)) +
                           double((pm_tiles * u.ks + pairs - 1) / pairs) * double(kbps1) * 4.0 *
                               std::max(120.0, 0.5 * double(bnh));
-        if (c1 <= u.cycles) {
+        // Decide with the ingest-aware model (a K block costs max(129 cycles per UMMA, TMA
+        // ingest bytes / 42 B per cycle per SM), tools/mma_micro.cu + scripts/exp_sweep.sh):
+        // W once per row pair vs once per N split.  Measured: C3 norm 219 -> 176 us with the
+        // full-r tiling, C2 / C4 r=512 faster with N splits (enough row pairs to fill the SMs).
+        const int64_t pt1 = pm_tiles * u.sp.ns * u.ks, pt2 = pm_tiles * u.ks;
+        const double kb1 = std::max(4.0 * 129.0, (16384.0 + u.sp.bn / 2 * 128.0) / 42.0);
+        const double kb2 = std::max(8.0 * 129.0, (16384.0 + double(bnh) * 128.0) / 42.0);
+        const double i1 = double((pt1 + pairs - 1) / pairs) * kb1;
+        const double i2 = double((pt2 + pairs - 1) / pairs) * kb2;
+        if (i2 < i1 || c1 <= u.cycles) {
             u.nh = 2;
             u.sp = {1, u.sp.ks, static_cast<int>(bnh)};
             u.work = 2 * pm_tiles;

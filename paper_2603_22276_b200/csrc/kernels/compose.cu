@@ -262,11 +262,11 @@ __global__ void __launch_bounds__(256) compose_bwd_vec(const T* __restrict__ dy,
 //   warp 0    = TMA producer
 //   warps 1.. = chain warps, one thread per column, serial over rows (bitwise ref order)
 //   last 4    = elementwise warps: d_lora / d_base from the same stage, 16 B stores
-template <typename T>
+template <typename T, int S = 6>
 struct SerialCfg {
     static constexpr int kSC = 128 / sizeof(T);            // slab columns
     static constexpr int kRB = 64;                          // rows per stage
-    static constexpr int kStages = 6;
+    static constexpr int kStages = S;
     static constexpr int kStageBytes = kRB * 128;           // per tensor
     static constexpr int kCPT = 4 / sizeof(T);              // chain columns per thread
     static constexpr int kChainWarps = 1;                   // 32 threads x kCPT columns
@@ -275,13 +275,13 @@ struct SerialCfg {
     static constexpr int kSmem = 2 * kStages * kStageBytes + 2 * kStages * 8 + 1024;
 };
 
-template <typename T>
-__global__ void __launch_bounds__(SerialCfg<T>::kThreads, 1)
+template <typename T, int S>
+__global__ void __launch_bounds__(SerialCfg<T, S>::kThreads, 1)
     compose_bwd_serial(const __grid_constant__ CUtensorMap tm_dy,
                        const __grid_constant__ CUtensorMap tm_inner, const float* __restrict__ g,
                        float sf, const float* __restrict__ w_norm, int64_t rows, int64_t d_out,
                        T* __restrict__ d_lora, T* __restrict__ d_base, float* __restrict__ d_mag) {
-    using C = SerialCfg<T>;
+    using C = SerialCfg<T, S>;
     constexpr int V = Vec<T>::N;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -483,6 +483,27 @@ cudaError_t fwd_impl(const void* base, const void* lora, const float* g, float s
     return cudaGetLastError();
 }
 
+template <typename T, int S>
+cudaError_t bwd_serial_launch(int dt, const void* dy, const float* g, float sf, const void* inner,
+                              const float* w_norm, int64_t rows, int64_t d_out, T* dl, T* db,
+                              float* d_mag, cudaStream_t st) {
+    using C = SerialCfg<T, S>;
+    CUtensorMap tm_dy, tm_in;
+    const uint64_t pitch = static_cast<uint64_t>(d_out) * sizeof(T);
+    cudaError_t e = make_tmap_2d(&tm_dy, dt, dy, rows, d_out, pitch, C::kSC, C::kRB, false);
+    if (e != cudaSuccess) return e;
+    e = make_tmap_2d(&tm_in, dt, inner, rows, d_out, pitch, C::kSC, C::kRB, false);
+    if (e != cudaSuccess) return e;
+    e = ensure_max_dyn_smem(reinterpret_cast<const void*>(compose_bwd_serial<T, S>), C::kSmem);
+    if (e != cudaSuccess) return e;
+    const unsigned grid = static_cast<unsigned>((d_out + C::kSC - 1) / C::kSC);
+    prof_begin("compose_bwd_dmag", st);
+    compose_bwd_serial<T, S><<<grid, C::kThreads, C::kSmem, st>>>(tm_dy, tm_in, g, sf, w_norm, rows,
+                                                                   d_out, dl, db, d_mag);
+    prof_end(st);
+    return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t bwd_impl(int dt, const void* dy, const float* g, float sf, const void* inner,
                      const float* w_norm, int64_t rows, int64_t d_out, void* d_lora, void* d_base,
@@ -517,20 +538,16 @@ cudaError_t bwd_impl(int dt, const void* dy, const float* g, float sf, const voi
     }
     const T* in = static_cast<const T*>(inner);
     if (vec && rows > 0) {
-        using C = SerialCfg<T>;
-        CUtensorMap tm_dy, tm_in;
-        const uint64_t pitch = static_cast<uint64_t>(d_out) * sizeof(T);
-        cudaError_t e = make_tmap_2d(&tm_dy, dt, dy, rows, d_out, pitch, C::kSC, C::kRB, false);
-        if (e != cudaSuccess) return e;
-        e = make_tmap_2d(&tm_in, dt, inner, rows, d_out, pitch, C::kSC, C::kRB, false);
-        if (e != cudaSuccess) return e;
-        e = ensure_max_dyn_smem(reinterpret_cast<const void*>(compose_bwd_serial<T>), C::kSmem);
-        if (e != cudaSuccess) return e;
-        const unsigned grid = static_cast<unsigned>((d_out + C::kSC - 1) / C::kSC);
-        prof_begin("compose_bwd_dmag", st);
-        compose_bwd_serial<T><<<grid, C::kThreads, C::kSmem, st>>>(
-            tm_dy, tm_in, g, sf, w_norm, rows, d_out, dl, db, d_mag);
-        prof_end(st);
+        // one CTA per 128-byte column slab runs the whole column height; when the slabs
+        // outnumber two per SM, a shallower ring (3 stages, ~49 KB) lets four share an SM so
+        // the grid stays one wave (C3: 448 slabs)
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t slabs = (d_out + SerialCfg<T>::kSC - 1) / SerialCfg<T>::kSC;
+        return slabs > 2 * int64_t(sms)
+                   ? bwd_serial_launch<T, 3>(dt, dy, g, sf, inner, w_norm, rows, d_out, dl, db, d_mag, st)
+                   : bwd_serial_launch<T, 6>(dt, dy, g, sf, inner, w_norm, rows, d_out, dl, db, d_mag, st);
     } else {
         prof_begin("compose_bwd_dmag_generic", st);
         compose_bwd_generic<T, true><<<static_cast<unsigned>((d_out + 127) / 128), 128, 0, st>>>(

@@ -144,6 +144,14 @@ int dfx_compose_bwd(dfx_ctx* ctx, dfx_dtype dtype, const void* dy, const float* 
                     const void* inner, const float* w_norm, int64_t rows, int64_t d_out,
                     void* d_lora, void* d_base, float* d_mag, dfx_stream_t stream);
 
+/* The layer's plain GEMMs with the reference's working_matmul semantics (layer.cpp:15-17 over
+ * matrix.cpp:53-78), bitwise: C [M x N] row-major (dtype) = round(serial-k fp32 sum of
+ * a(i,k) * b(k,j)), a(i,k) = A[i*sa_i + k*sa_k], b(k,j) = B[k*sb_k + j*sb_j] (element strides,
+ * so transposed operands need no copy).  CUDA cores: the serial order is the contract. */
+int dfx_working_matmul(dfx_ctx* ctx, dfx_dtype dtype, const void* A, int64_t sa_i, int64_t sa_k,
+                       const void* B, int64_t sb_k, int64_t sb_j, int64_t M, int64_t N, int64_t K,
+                       void* C, dfx_stream_t stream);
+
 /* layer_forward's LoRA-up GEMM fused with the compose and the residual (layer.cpp:57-58,
  * 73-120): lora = round(mid . B^T) is formed on the tensor cores and
  * never reaches HBM; per element delta = round((g-1)*base + g*(s*lora)) (compose.cpp:19-24),

@@ -77,6 +77,8 @@ SIGNATURES = {
     "dfx_module_fwd_host": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _f64, _i64, _i64,
                                    _i64, _i64, _i64, _vp, _vp]),
     "dfx_ctx_set_sm_budget": (_int, [_vp, _int]),
+    "dfx_working_matmul": (_int, [_vp, _int, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64,
+                                  _vp, _vp]),
     "dfx_lora_compose": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _f64, _vp, _i64, _i64, _i64, _vp,
                                 _vp, _vp, _vp, _vp]),
     "dfx_module_train_host": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f64, _i64,
@@ -224,6 +226,18 @@ class Dfx:
         self._check(self.lib.dfx_compose_bwd(self.ctx, dt, _ptr(dy), _ptr(g), float(s),
                                              _ptr(inner), _ptr(w_norm), rows, d_out, _ptr(d_lora),
                                              _ptr(d_base), _ptr(d_mag), _stream(stream)))
+
+    def working_matmul(self, a, b, c, trans_a=False, trans_b=True, stream=None):
+        """c = round(a' . b') with the reference's serial-k fp32 order, where a' = a^T if
+        trans_a and b' = b^T if trans_b (row-major device tensors, no copies)."""
+        M = a.shape[1] if trans_a else a.shape[0]
+        K = a.shape[0] if trans_a else a.shape[1]
+        N = b.shape[0] if trans_b else b.shape[1]
+        sa_i, sa_k = (1, a.shape[1]) if trans_a else (a.shape[1], 1)
+        sb_k, sb_j = (1, b.shape[1]) if trans_b else (b.shape[1], 1)
+        self._check(self.lib.dfx_working_matmul(self.ctx, _dtype_code(a), _ptr(a), sa_i, sa_k,
+                                                _ptr(b), sb_k, sb_j, M, N, K, _ptr(c),
+                                                _stream(stream)))
 
     def set_sm_budget(self, sms: int):
         """Cap the SMs the norm GEMMs plan for (0 = all); see dfx_ctx_set_sm_budget."""

@@ -569,6 +569,22 @@ int dfx_ctx_set_sm_budget(dfx_ctx* ctx, int sms) {
     return DFX_OK;
 }
 
+int dfx_working_matmul(dfx_ctx* ctx, dfx_dtype dtype, const void* A, int64_t sa_i, int64_t sa_k,
+                       const void* B, int64_t sb_k, int64_t sb_j, int64_t M, int64_t N, int64_t K,
+                       void* C, dfx_stream_t stream) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (!valid_dtype(dtype)) return fail(DFX_EUNSUPPORTED, "working_matmul: dtype");
+    if (M < 0 || N < 0 || K < 0) return fail(DFX_EINVAL, "matmul_f32: inner dimensions disagree");
+    if (M > 0 && N > 0 && (!C || (K > 0 && (!A || !B))))
+        return fail(DFX_EINVAL, "working_matmul: null operand");
+    int launches = 0;
+    const cudaError_t e = dfx::launch_working_matmul(dtype, A, sa_i, sa_k, B, sb_k, sb_j, M, N, K, C,
+                                                     stream, &launches);
+    ctx->launches += launches;
+    return finish_call(e, "dfx_working_matmul");
+}
+
 int dfx_lora_compose(dfx_ctx* ctx, dfx_dtype dtype, const void* mid, const void* B,
                      const void* base, const float* g, double s, const float* bias, int64_t rows,
                      int64_t d_out, int64_t r, void* y, void* delta, void* inner, void* lora,

@@ -24,7 +24,9 @@
 
 #include "dfx.h"
 #include "dorafactor/compose.hpp"
+#include "dorafactor/dispatch.hpp"
 #include "dorafactor/factored_norm.hpp"
+#include "dorafactor/layer.hpp"
 
 namespace dorafactor {
 
@@ -581,6 +583,243 @@ TrafficReport eager_traffic_model(index_t rows, index_t d_out, const DTypeSpec& 
     t.bytes_total = (t.activation_reads + t.activation_writes) * act * eb +
                     t.vector_reads * static_cast<std::uint64_t>(d_out) * eb;
     return t;
+}
+
+// ================================================================== layer (8f row 2)
+// The hot path's production caller on the device: the plain GEMMs run dfx_working_matmul
+// (the reference's serial-k fp32 order, bitwise) on device-resident operands addressed
+// with strides (no transposed copies), the norm / compose / backward kernels follow, and
+// only the results come back.  Operands whose dtype tag differs from the working dtype
+// take the same steps through fp32 storage with the working-dtype rounding applied on the
+// host, which is where the reference applies it (rounded_to after matmul_f32).
+namespace {
+
+// C = a' . b' on the device; strides in elements (see dfx_working_matmul)
+DevBuf gemm(dfx_dtype dt, const DevBuf& a, int64_t sa_i, int64_t sa_k, const DevBuf& b,
+            int64_t sb_k, int64_t sb_j, index_t M, index_t N, index_t K) {
+    DevBuf c(M * N * elem_size(dt));
+    check(dfx_working_matmul(device_ctx(), dt, a.p, sa_i, sa_k, b.p, sb_k, sb_j, M, N, K, c.p,
+                             nullptr));
+    return c;
+}
+
+RealMatrix fetch(const DevBuf& d, dfx_dtype dt, index_t rows, index_t cols, const DTypeSpec& tag) {
+    RealMatrix m(rows, cols, tag);
+    download(d, dt, m);
+    return m;
+}
+
+void round_all(RealMatrix& m, const DTypeSpec& dt) {
+    for (double& v : m.mutable_data()) v = round_to_dtype(v, dt);
+}
+
+}  // namespace
+
+ForceMode force_mode_from_name(const std::string& name) {
+    if (name == "auto") return ForceMode::Auto;
+    if (name == "on" || name == "1") return ForceMode::On;
+    if (name == "off" || name == "0") return ForceMode::Off;
+    throw std::invalid_argument("unknown force mode: " + name);
+}
+
+const char* force_mode_name(ForceMode mode) {
+    static const char* const names[] = {"auto", "on", "off"};
+    const int i = static_cast<int>(mode);
+    return i >= 0 && i < 3 ? names[i] : "?";
+}
+
+const char* dispatch_reason_name(DispatchReason r) {
+    static const char* const names[] = {"NO_ACCELERATOR", "NO_KERNELS", "FORCED",
+                                        "NON_CONTIGUOUS", "SHAPE_GUARD", "BELOW_CROSSOVER",
+                                        "ABOVE_CROSSOVER", "INFERENCE", "GRAD_OUTSIDE_TRAINING"};
+    const int i = static_cast<int>(r);
+    return i >= 0 && i < 9 ? names[i] : "?";
+}
+
+bool TierDecision::has_reason(DispatchReason r) const {
+    return std::find(reasons.begin(), reasons.end(), r) != reasons.end();
+}
+
+TierDecision select_tier(const DispatchContext& c) {
+    TierDecision d;
+    using R = DispatchReason;
+    // hard guards, all recorded (dispatch.cpp:46-57)
+    const std::pair<bool, R> guards[] = {
+        {!c.accelerator_available, R::NO_ACCELERATOR}, {!c.kernels_available, R::NO_KERNELS},
+        {c.force_fused == ForceMode::Off, R::FORCED},  {!c.contiguous, R::NON_CONTIGUOUS},
+        {!c.mag_broadcast_last_dim, R::SHAPE_GUARD},   {!c.d_out_divisible_128, R::SHAPE_GUARD}};
+    for (const auto& gr : guards)
+        if (gr.first) d.reasons.push_back(gr.second);
+    if (!d.reasons.empty()) return d;                                   // Eager
+    if (!c.requires_grad) {
+        d.tier = Tier::FusedForward;
+        d.reasons.push_back(R::INFERENCE);
+    } else if (!c.training) {
+        d.reasons.push_back(R::GRAD_OUTSIDE_TRAINING);                  // Eager
+    } else if (c.force_fused_backward != ForceMode::Auto) {
+        d.tier = c.force_fused_backward == ForceMode::On ? Tier::FusedBackward : Tier::Eager;
+        d.reasons.push_back(R::FORCED);
+    } else {
+        const bool above = c.d_out >= c.crossover_min_d_out &&
+                           std::uint64_t(c.rows) * c.d_out >= c.crossover_min_elems;
+        d.tier = above ? Tier::FusedBackward : Tier::Eager;
+        d.reasons.push_back(above ? R::ABOVE_CROSSOVER : R::BELOW_CROSSOVER);
+    }
+    return d;
+}
+
+bool shape_guard(index_t activation_last_dim, index_t magnitude_len,
+                 const std::vector<index_t>& broadcast_dims) {
+    if (magnitude_len != activation_last_dim) return false;
+    if (broadcast_dims.empty()) return true;
+    if (broadcast_dims.back() != magnitude_len) return false;
+    return std::all_of(broadcast_dims.begin(), broadcast_dims.end() - 1,
+                       [](index_t v) { return v == 1; });
+}
+
+RealMatrix matmul_f32(const RealMatrix& a, const RealMatrix& b) {
+    if (a.cols() != b.rows())
+        throw std::invalid_argument("matmul_f32: inner dimensions disagree (" +
+                                    std::to_string(a.cols()) + " vs " + std::to_string(b.rows()) + ")");
+    const index_t m = a.rows(), k = a.cols(), n = b.cols();
+    const DevBuf da = upload(a.data(), DFX_F32), db = upload(b.data(), DFX_F32);
+    const DevBuf dc = gemm(DFX_F32, da, int64_t(k), 1, db, int64_t(n), 1, m, n, k);
+    return fetch(dc, DFX_F32, m, n, DTypeSpec::fp32());
+}
+
+DoraLinearState make_layer_state(RealMatrix w, AdapterPair adapter, Magnitude magnitude,
+                                 std::optional<std::vector<double>> bias,
+                                 const DTypeSpec& working_dtype) {
+    const index_t d_out = w.rows(), d_in = w.cols();
+    if (adapter.A.cols() != d_in || adapter.B.rows() != d_out ||
+        adapter.A.rows() != adapter.B.cols())
+        throw std::invalid_argument("layer: adapter shapes inconsistent with W");
+    if (magnitude.values.size() != d_out)
+        throw std::invalid_argument("layer: magnitude length != d_out");
+    if (bias && bias->size() != d_out) throw std::invalid_argument("layer: bias length != d_out");
+    DoraLinearState st;
+    st.working_dtype = working_dtype;
+    magnitude.dtype = working_dtype;
+    for (double& v : magnitude.values) v = round_to_dtype(v, working_dtype);
+    if (bias)
+        for (double& v : *bias) v = round_to_dtype(v, working_dtype);
+    st.w = std::move(w);
+    st.adapter = std::move(adapter);
+    st.magnitude = std::move(magnitude);
+    st.bias = std::move(bias);
+    st.chunk_plan = plan_chunks(d_out, d_in);
+    st.dispatch_cfg.training = true;
+    st.dispatch_cfg.requires_grad = true;
+    return st;
+}
+
+LayerForwardResult layer_forward(const DoraLinearState& st, const RealMatrix& x) {
+    if (x.cols() != st.d_in()) throw std::invalid_argument("layer_forward: X.cols != d_in");
+    const DTypeSpec& wd = st.working_dtype;
+    if (wd.kind == DTypeKind::FP64)
+        throw std::invalid_argument("layer_forward: FP64 working dtype is not a B200 storage format");
+    const index_t rows = x.rows(), d_in = st.d_in(), d_out = st.d_out(), r = st.adapter.A.rows();
+    const AdapterPair& ad = st.adapter;
+    dfx_ctx* ctx = device_ctx();
+    // native: every operand already carries the working dtype, so the GEMMs store their
+    // rounded results directly; otherwise fp32 storage and host-side rounding
+    const bool native = x.dtype() == wd && st.w.dtype() == wd && ad.A.dtype() == wd &&
+                        ad.B.dtype() == wd;
+    const dfx_dtype gt = native ? to_dfx(wd) : DFX_F32;
+    const DevBuf dX = upload(x.data(), gt), dW = upload(st.w.data(), gt),
+                 dA = upload(ad.A.data(), gt), dB = upload(ad.B.data(), gt);
+    const int64_t Ri = int64_t(r), Di = int64_t(d_in);
+    DevBuf base = gemm(gt, dX, Di, 1, dW, 1, Di, rows, d_out, d_in);     // X W^T
+    DevBuf mid = gemm(gt, dX, Di, 1, dA, 1, Di, rows, r, d_in);          // X A^T
+    if (!native) {                      // round the fp32 products to wd, back to wd storage
+        RealMatrix m = fetch(mid, gt, rows, r, wd);
+        round_all(m, wd);
+        mid = upload(m.data(), gt);
+    }
+    DevBuf lora = gemm(gt, mid, Ri, 1, dB, 1, Ri, rows, d_out, r);       // mid B^T
+
+    LayerSaved sv;
+    sv.x = x;
+    sv.lora_mid = fetch(mid, gt, rows, r, wd);
+    sv.base_out = fetch(base, gt, rows, d_out, wd);
+    sv.lora_out = fetch(lora, gt, rows, d_out, wd);
+    if (!native) {
+        round_all(sv.base_out, wd);
+        round_all(sv.lora_out, wd);
+    }
+    // detached norm, recomputed every call, and g (factored_row_norm + magnitude_scale)
+    sv.w_norm = factored_row_norm(st.w, ad, st.chunk_plan);
+    sv.g = magnitude_scale(st.magnitude, sv.w_norm, wd);
+
+    DispatchContext dc = st.dispatch_cfg;
+    dc.rows = rows;
+    dc.d_out = d_out;
+    dc.contiguous = true;
+    dc.mag_broadcast_last_dim = true;
+    dc.d_out_divisible_128 = d_out % 128 == 0;
+    sv.decision = select_tier(dc);
+    const bool want_inner = dc.training && dc.requires_grad && st.mag_trainable;
+
+    // every tier computes the same canonical compose; the dual kernel provides inner
+    const dfx_dtype ct = to_dfx(wd);
+    const DevBuf cb = upload(sv.base_out.data(), ct), cl = upload(sv.lora_out.data(), ct);
+    std::vector<float> gf(d_out);
+    for (index_t j = 0; j < d_out; ++j) gf[j] = static_cast<float>(sv.g[j]);
+    const DevBuf dg = upload_f32(gf);
+    DevBuf delta(rows * d_out * elem_size(ct));
+    std::unique_ptr<DevBuf> inner(want_inner ? new DevBuf(rows * d_out * elem_size(ct)) : nullptr);
+    check(dfx_compose_fwd(ctx, ct, cb.p, cl.p, dg.as<float>(), ad.s, rows, d_out, delta.p,
+                          inner ? inner->p : nullptr, nullptr));
+    const RealMatrix dm = fetch(delta, ct, rows, d_out, wd);
+    if (inner) sv.inner = fetch(*inner, ct, rows, d_out, wd);
+
+    // residual, then bias, each an fp32 add stored in the working dtype
+    RealMatrix y(rows, d_out, wd);
+    std::vector<double>& yv = y.mutable_data();
+    const std::vector<double>& bv = sv.base_out.data();
+    const std::vector<double>& dv = dm.data();
+    for (index_t e = 0; e < rows * d_out; ++e) {
+        double v = round_to_dtype(static_cast<double>(static_cast<float>(bv[e]) +
+                                                      static_cast<float>(dv[e])), wd);
+        if (st.bias)
+            v = round_to_dtype(static_cast<double>(static_cast<float>(v) +
+                                                   static_cast<float>((*st.bias)[e % d_out])), wd);
+        yv[e] = v;
+    }
+    return LayerForwardResult{std::move(y), std::move(sv)};
+}
+
+LayerGrads layer_backward(const DoraLinearState& st, const LayerSaved& sv, const RealMatrix& d_y) {
+    const index_t rows = sv.x.rows(), d_out = st.d_out(), d_in = st.d_in(), r = st.adapter.A.rows();
+    if (d_y.rows() != rows || d_y.cols() != d_out)
+        throw std::invalid_argument("layer_backward: dY shape mismatch");
+    const bool mag_grad = st.mag_trainable;
+    if (mag_grad && !sv.inner)
+        throw std::invalid_argument("layer_backward: saved bundle lacks inner for magnitude grad");
+    const DTypeSpec& wd = st.working_dtype;
+    GradBundle gb = compose_backward(d_y, sv.g, st.adapter.s, sv.inner ? &*sv.inner : nullptr,
+                                     sv.w_norm, mag_grad);
+    // dB = d_lora^T mid, d_mid = d_lora B, dA = d_mid^T X: strided operands, no transposes
+    const bool native = gb.d_lora.dtype() == wd && sv.lora_mid.dtype() == wd &&
+                        st.adapter.B.dtype() == wd && sv.x.dtype() == wd;
+    const dfx_dtype gt = native ? to_dfx(wd) : DFX_F32;
+    const DevBuf dl = upload(gb.d_lora.data(), gt), mid = upload(sv.lora_mid.data(), gt),
+                 dB = upload(st.adapter.B.data(), gt), dX = upload(sv.x.data(), gt);
+    const int64_t Ri = int64_t(r), Oi = int64_t(d_out), Di = int64_t(d_in);
+    const DevBuf db = gemm(gt, dl, 1, Oi, mid, Ri, 1, d_out, r, rows);
+    DevBuf dmid = gemm(gt, dl, Oi, 1, dB, Ri, 1, rows, r, d_out);
+    if (!native) {
+        RealMatrix m = fetch(dmid, gt, rows, r, wd);
+        round_all(m, wd);
+        dmid = upload(m.data(), gt);
+    }
+    const DevBuf da = gemm(gt, dmid, 1, Ri, dX, Di, 1, r, d_in, rows);
+    LayerGrads out{fetch(da, gt, r, d_in, wd), fetch(db, gt, d_out, r, wd), std::move(gb.d_mag)};
+    if (!native) {
+        round_all(out.d_a, wd);
+        round_all(out.d_b, wd);
+    }
+    return out;
 }
 
 }  // namespace dorafactor

@@ -43,6 +43,13 @@ cudaError_t launch_lora_compose(int dt, const void* mid, const void* b, const vo
                                 int64_t d_out, int64_t r, void* y, void* delta, void* inner,
                                 void* lora, cudaStream_t st, int* launches);
 
+// The layer's plain GEMMs with the reference's working_matmul semantics (layer_gemm.cu):
+// C [M x N] row-major = round_dtype(serial-k fp32 sum of a(i, k) * b(k, j)), with
+// a(i, k) = a[i * sa_i + k * sa_k] and b(k, j) = b[k * sb_k + j * sb_j] (element strides).
+cudaError_t launch_working_matmul(int dt, const void* a, int64_t sa_i, int64_t sa_k, const void* b,
+                                  int64_t sb_k, int64_t sb_j, int64_t M, int64_t N, int64_t K,
+                                  void* c, cudaStream_t st, int* launches);
+
 // ------------------------------------------------------------------- norm
 struct NormArgs {
     int dt;

@@ -1,19 +1,23 @@
 // test_dropin.cpp — the reference's hot-path unit tests, restated against the B200
 // drop-in (libdorafactor_b200.so).  Each TEST names the reference case it mirrors
-// (proj/tests/test_factored_norm.cpp, test_compose.cpp, acceptance.cpp).  Expected
+// (proj/tests/test_factored_norm.cpp, test_compose.cpp, test_dispatch.cpp, test_layer.cpp,
+// acceptance.cpp).  Expected
 // values are computed here on the host with plain fp32/fp64 arithmetic
 // (-ffp-contract=off), so bitwise checks compare the GPU against the reference's
 // arithmetic contract, not against itself.
 //
 // Run on a B200: tests/cpp/test_dropin [filter]   (driven by tests/test_gpu_dropin.py)
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
 
 #include "dorafactor/compose.hpp"
+#include "dorafactor/dispatch.hpp"
 #include "dorafactor/factored_norm.hpp"
+#include "dorafactor/layer.hpp"
 #include "mini_test.hpp"
 
 using namespace dorafactor;
@@ -461,6 +465,361 @@ TEST("compose: eager traffic model (test_compose.cpp:204)") {
                          static_cast<double>(f.traffic.bytes_total);
     CHECK(ratio >= 2.5);
     CHECK(ratio <= 4.0);
+}
+
+// ------------------------------------------------------------------ test_dispatch.cpp
+namespace {
+
+DispatchContext dctx(bool training, bool requires_grad, index_t rows, index_t d_out) {
+    DispatchContext c;
+    c.training = training;
+    c.requires_grad = requires_grad;
+    c.rows = rows;
+    c.d_out = d_out;
+    c.d_out_divisible_128 = d_out % 128 == 0;
+    return c;
+}
+
+}  // namespace
+
+TEST("dispatch: tier basics and the inclusive crossover (test_dispatch.cpp:22)") {
+    const TierDecision small = select_tier(dctx(true, true, 4096, 512));
+    CHECK(small.tier == Tier::Eager);
+    CHECK(small.has_reason(DispatchReason::BELOW_CROSSOVER));
+    CHECK(select_tier(dctx(true, true, 4096, 4096)).tier == Tier::FusedBackward);
+    CHECK(select_tier(dctx(false, false, 16, 4096)).tier == Tier::FusedForward);
+    CHECK(select_tier(dctx(true, true, 6144, 2048)).tier == Tier::FusedBackward);
+    CHECK(select_tier(dctx(true, true, 6143, 2048)).tier == Tier::Eager);
+}
+
+TEST("dispatch: force precedence (test_dispatch.cpp:42)") {
+    for (int training = 0; training < 2; ++training)
+        for (index_t d_out : {index_t(512), index_t(8192)}) {
+            DispatchContext c = dctx(training, training, 8192, d_out);
+            c.force_fused = ForceMode::Off;
+            const TierDecision d = select_tier(c);
+            CHECK(d.tier == Tier::Eager);
+            CHECK(d.has_reason(DispatchReason::FORCED));
+        }
+    DispatchContext c = dctx(true, true, 2, 128);
+    c.force_fused_backward = ForceMode::On;
+    CHECK(select_tier(c).tier == Tier::FusedBackward);
+    c.force_fused_backward = ForceMode::Off;
+    CHECK(select_tier(c).tier == Tier::Eager);
+    CHECK(force_mode_from_name("1") == ForceMode::On);
+    CHECK(std::strcmp(force_mode_name(ForceMode::Auto), "auto") == 0);
+    CHECK(std::strcmp(dispatch_reason_name(DispatchReason::SHAPE_GUARD), "SHAPE_GUARD") == 0);
+    CHECK_THROWS_AS(force_mode_from_name("sometimes"), std::invalid_argument);
+}
+
+TEST("dispatch: monotonic crossover, totality, fleet fraction (test_dispatch.cpp:59-110)") {
+    bool seen = false;
+    for (index_t rows = 128; rows <= 16384; rows *= 2)
+        for (index_t d_out = 128; d_out <= 16384; d_out *= 2)
+            if (select_tier(dctx(true, true, rows, d_out)).tier == Tier::FusedBackward) {
+                CHECK(select_tier(dctx(true, true, rows * 2, d_out)).tier == Tier::FusedBackward);
+                CHECK(select_tier(dctx(true, true, rows, d_out * 2)).tier == Tier::FusedBackward);
+                seen = true;
+            }
+    CHECK(seen);
+    for (std::uint64_t trial = 0; trial < 500; ++trial) {
+        const std::uint64_t h = derive_seed(99, trial);
+        DispatchContext c;
+        c.training = h & 1;
+        c.requires_grad = h & 2;
+        c.accelerator_available = h & 4;
+        c.kernels_available = h & 8;
+        c.contiguous = h & 16;
+        c.mag_broadcast_last_dim = h & 32;
+        c.force_fused = static_cast<ForceMode>((h >> 6) % 3);
+        c.force_fused_backward = static_cast<ForceMode>((h >> 8) % 3);
+        c.rows = 1 + (h >> 10) % 10000;
+        c.d_out = 1 + (h >> 24) % 10000;
+        c.d_out_divisible_128 = c.d_out % 128 == 0;
+        const TierDecision d = select_tier(c);
+        CHECK(static_cast<int>(d.tier) >= 1 && static_cast<int>(d.tier) <= 3);
+        if (d.tier == Tier::Eager) CHECK(!d.reasons.empty());
+        if (d.tier == Tier::FusedBackward) CHECK(c.training);
+        if (d.tier == Tier::FusedForward) CHECK(!c.requires_grad);
+    }
+    int tier1 = 0;
+    for (index_t d_out : {4096, 512, 512, 4096, 11008, 4096, 4096})
+        tier1 += select_tier(dctx(true, true, 4096, d_out)).tier == Tier::FusedBackward;
+    CHECK(tier1 == 5);
+}
+
+TEST("dispatch: shape guard (test_dispatch.cpp:123)") {
+    CHECK(shape_guard(4096, 4096, {}));
+    CHECK(shape_guard(4096, 4096, {1, 1, 4096}));
+    CHECK(!shape_guard(7, 64, {1, 64, 1, 1}));
+    CHECK(!shape_guard(4096, 2048, {}));
+    CHECK(!shape_guard(64, 64, {2, 1, 64}));
+    CHECK(shape_guard(64, 64, {64}));
+}
+
+// --------------------------------------------------------------------- test_layer.cpp
+namespace {
+
+DoraLinearState layer_state(std::uint64_t seed, index_t d_out = 12, index_t d_in = 18,
+                            index_t r = 3, bool with_bias = true,
+                            const DTypeSpec& dt = DTypeSpec::fp32()) {
+    RealMatrix w = gaussian_fixture(d_out, d_in, 0.0, 0.5, derive_seed(seed, 0), dt);
+    AdapterPair ad{gaussian_fixture(r, d_in, 0.0, 0.5, derive_seed(seed, 1), dt),
+                   gaussian_fixture(d_out, r, 0.0, 0.5, derive_seed(seed, 2), dt),
+                   2.0 / std::sqrt(static_cast<double>(r))};
+    Magnitude mag{gaussian_vector(d_out, 1.5, 0.2, derive_seed(seed, 3)), dt};
+    std::optional<std::vector<double>> bias;
+    if (with_bias) bias = gaussian_vector(d_out, 0.0, 0.5, derive_seed(seed, 4));
+    return make_layer_state(std::move(w), std::move(ad), std::move(mag), std::move(bias), dt);
+}
+
+// the reference's working_matmul on the host: serial-k fp32 products and sums, rounded
+RealMatrix host_matmul(const RealMatrix& a, const RealMatrix& b, bool tb, const DTypeSpec& dt) {
+    const index_t m = a.rows(), k = a.cols(), n = tb ? b.rows() : b.cols();
+    RealMatrix c(m, n, dt);
+    for (index_t i = 0; i < m; ++i)
+        for (index_t j = 0; j < n; ++j) {
+            float acc = 0.0f;
+            for (index_t q = 0; q < k; ++q)
+                acc += static_cast<float>(a(i, q)) * static_cast<float>(tb ? b(j, q) : b(q, j));
+            c.set(i, j, round_to_dtype(acc, dt));
+        }
+    return c;
+}
+
+RealMatrix host_transpose(const RealMatrix& a) {
+    RealMatrix t(a.cols(), a.rows(), a.dtype());
+    for (index_t i = 0; i < a.rows(); ++i)
+        for (index_t j = 0; j < a.cols(); ++j) t.set(j, i, a(i, j));
+    return t;
+}
+
+// fp64 DoRA forward with the norm from the dense fp64 statement (reference.cpp oracle_forward)
+RealMatrix host_oracle_forward(const DoraLinearState& st, const RealMatrix& x) {
+    const std::vector<double> wn = dense_norm_f64(st.w, st.adapter);
+    RealMatrix y(x.rows(), st.d_out(), DTypeSpec::fp64());
+    for (index_t i = 0; i < x.rows(); ++i)
+        for (index_t o = 0; o < st.d_out(); ++o) {
+            double base = 0.0, lora = 0.0;
+            for (index_t k = 0; k < st.d_in(); ++k) base += x(i, k) * st.w(o, k);
+            for (index_t l = 0; l < st.adapter.rank(); ++l) {
+                double mid = 0.0;
+                for (index_t k = 0; k < st.d_in(); ++k) mid += x(i, k) * st.adapter.A(l, k);
+                lora += mid * st.adapter.B(o, l);
+            }
+            const double g = st.magnitude.values[o] / std::max(wn[o], 1e-12);
+            y.set(i, o, g * (base + st.adapter.s * lora) + (st.bias ? (*st.bias)[o] : 0.0));
+        }
+    return y;
+}
+
+}  // namespace
+
+TEST("layer: matmul_f32 is the serial fp32 product (matrix.cpp:53)") {
+    const RealMatrix a = gaussian_fixture(37, 45, 0.0, 1.0, 201, DTypeSpec::fp32());
+    const RealMatrix b = gaussian_fixture(45, 29, 0.0, 1.0, 202, DTypeSpec::fp32());
+    CHECK(same_bits(matmul_f32(a, b), host_matmul(a, b, false, DTypeSpec::fp32())));
+    CHECK_THROWS_AS(matmul_f32(a, a), std::invalid_argument);
+}
+
+TEST("layer: forward at adapter init reduces to the frozen layer (test_layer.cpp:33)") {
+    DoraLinearState st = layer_state(1);
+    for (double& v : st.adapter.B.mutable_data()) v = 0.0;
+    st.magnitude.values = factored_row_norm(st.w, st.adapter, st.chunk_plan);
+    const RealMatrix x = gaussian_fixture(7, 18, 0.0, 1.0, 100);
+    const LayerForwardResult f = layer_forward(st, x);
+    for (double g : f.saved.g) CHECK(g == 1.0);
+    const RealMatrix base = matmul_f32(x, host_transpose(st.w));
+    for (index_t i = 0; i < 7; ++i)
+        for (index_t j = 0; j < st.d_out(); ++j)
+            CHECK(f.y(i, j) == static_cast<double>(static_cast<float>(base(i, j)) +
+                                                   static_cast<float>((*st.bias)[j])));
+}
+
+// The reference's bound, 1e-5 relative with a 1e-3 floor, does not hold for its own
+// arithmetic at y(6, 9) of this fixture: base 3.2030497 and delta -3.1896958 cancel to
+// 0.0133538395, which is exactly what the reference's layer_forward returns (oracle/_ref,
+// checked in this container), 3.8e-7 from the fp64 value.  Kept: the 1e-5 bound where no
+// cancellation happens, a cancellation-aware fp32 bound (a few ulps of the summands)
+// everywhere, and the reference's own value at (6, 9) bitwise.
+TEST("layer: forward matches the fp64 oracle (test_layer.cpp:52)") {
+    const DoraLinearState st = layer_state(2);
+    const RealMatrix x = gaussian_fixture(9, 18, 0.0, 1.0, 101);
+    const LayerForwardResult f = layer_forward(st, x);
+    const RealMatrix want = host_oracle_forward(st, x);
+    int loose = 0;
+    for (index_t i = 0; i < 9; ++i)
+        for (index_t j = 0; j < st.d_out(); ++j) {
+            const double err = std::fabs(f.y(i, j) - want(i, j)), g = f.saved.g[j];
+            const double b = std::fabs(f.saved.base_out(i, j)), l = std::fabs(f.saved.lora_out(i, j));
+            const double summands = b + std::fabs(g - 1.0) * b + std::fabs(g * st.adapter.s) * l;
+            loose += err > 1e-5 * std::max(std::fabs(want(i, j)), 1e-3);
+            CHECK(err <= 1e-5 * std::max(std::fabs(want(i, j)), 1e-3) + 0x1p-21 * summands);
+        }
+    std::printf("    %d of 108 outside the reference's plain bound (cancellation)\n", loose);
+    CHECK(loose <= 2);
+    CHECK(f.y(6, 9) == static_cast<double>(0.0133538395f));
+}
+
+// The reference case builds d_out = 24 and REQUIREs FusedBackward under a forced backward,
+// but its own select_tier records SHAPE_GUARD for d_out % 128 != 0 first (dispatch.cpp:52)
+// and returns Eager — checked by compiling dispatch.cpp alone.  Kept: that d_out = 24
+// resolves to Eager with SHAPE_GUARD, and the invariance itself on d_out = 128, where the
+// forced tiers really are taken.
+TEST("layer: tier invariance is bitwise, forward and backward (test_layer.cpp:65)") {
+    {
+        DoraLinearState s24 = layer_state(3, 24, 16, 4, false);
+        s24.dispatch_cfg.force_fused_backward = ForceMode::On;
+        const TierDecision d = layer_forward(s24, gaussian_fixture(11, 16, 0.0, 1.0, 102)).saved.decision;
+        CHECK(d.tier == Tier::Eager);
+        CHECK(d.has_reason(DispatchReason::SHAPE_GUARD));
+    }
+    DoraLinearState st = layer_state(3, 128, 16, 4, false);
+    const RealMatrix x = gaussian_fixture(11, 16, 0.0, 1.0, 102);
+    st.dispatch_cfg.force_fused_backward = ForceMode::On;
+    const LayerForwardResult t1 = layer_forward(st, x);
+    REQUIRE(t1.saved.decision.tier == Tier::FusedBackward);
+    st.dispatch_cfg.force_fused_backward = ForceMode::Off;
+    const LayerForwardResult t3 = layer_forward(st, x);
+    REQUIRE(t3.saved.decision.tier == Tier::Eager);
+    DoraLinearState inf = st;
+    inf.dispatch_cfg.training = false;
+    inf.dispatch_cfg.requires_grad = false;
+    const LayerForwardResult t2 = layer_forward(inf, x);
+    REQUIRE(t2.saved.decision.tier == Tier::FusedForward);
+    CHECK(same_bits(t1.y, t3.y));
+    CHECK(same_bits(t1.y, t2.y));
+    const RealMatrix dy = gaussian_fixture(11, 128, 0.0, 1.0, 103);
+    const LayerGrads g1 = layer_backward(st, t1.saved, dy), g3 = layer_backward(st, t3.saved, dy);
+    CHECK(same_bits(g1.d_a, g3.d_a));
+    CHECK(same_bits(g1.d_b, g3.d_b));
+    CHECK(*g1.d_mag == *g3.d_mag);
+}
+
+TEST("layer: bias is a pure post-add (test_layer.cpp:95)") {
+    const DoraLinearState wb = layer_state(4);
+    DoraLinearState nb = wb;
+    nb.bias.reset();
+    const RealMatrix x = gaussian_fixture(6, 18, 0.0, 1.0, 104);
+    const RealMatrix yb = layer_forward(wb, x).y, y0 = layer_forward(nb, x).y;
+    for (index_t i = 0; i < 6; ++i)
+        for (index_t j = 0; j < wb.d_out(); ++j)
+            CHECK(yb(i, j) == static_cast<double>(static_cast<float>(y0(i, j)) +
+                                                  static_cast<float>((*wb.bias)[j])));
+}
+
+TEST("layer: norm recomputed every forward (test_layer.cpp:111)") {
+    DoraLinearState st = layer_state(5);
+    const RealMatrix x = gaussian_fixture(4, 18, 0.0, 1.0, 105);
+    const std::vector<double> before = layer_forward(st, x).saved.w_norm;
+    st.w.set(0, 0, st.w(0, 0) + 2.0);
+    const std::vector<double> after = layer_forward(st, x).saved.w_norm;
+    CHECK(before != after);
+    CHECK(before[1] == after[1]);
+}
+
+TEST("layer: frozen magnitude, zero upstream grad, bundle validation (test_layer.cpp:121-222)") {
+    DoraLinearState st = layer_state(6);
+    st.mag_trainable = false;
+    st.dispatch_cfg.force_fused_backward = ForceMode::On;
+    const LayerForwardResult f = layer_forward(st, gaussian_fixture(5, 18, 0.0, 1.0, 106));
+    CHECK(!f.saved.inner.has_value());
+    CHECK(!layer_backward(st, f.saved, gaussian_fixture(5, 12, 0.0, 1.0, 107)).d_mag.has_value());
+
+    const DoraLinearState s7 = layer_state(7);
+    const LayerForwardResult f7 = layer_forward(s7, gaussian_fixture(5, 18, 0.0, 1.0, 108));
+    const LayerGrads z = layer_backward(s7, f7.saved, RealMatrix(5, 12, DTypeSpec::fp32()));
+    for (double v : z.d_a.data()) CHECK(v == 0.0);
+    for (double v : z.d_b.data()) CHECK(v == 0.0);
+    for (double v : *z.d_mag) CHECK(v == 0.0);
+
+    const DoraLinearState s9 = layer_state(9);
+    LayerForwardResult f9 = layer_forward(s9, gaussian_fixture(4, 18, 0.0, 1.0, 110));
+    f9.saved.inner.reset();
+    CHECK_THROWS_AS(layer_backward(s9, f9.saved, gaussian_fixture(4, 12, 0.0, 1.0, 111)),
+                    std::invalid_argument);
+    CHECK_THROWS_AS(layer_backward(s9, f9.saved, gaussian_fixture(5, 12, 0.0, 1.0, 111)),
+                    std::invalid_argument);
+    CHECK_THROWS_AS(layer_forward(s9, gaussian_fixture(4, 17, 0.0, 1.0, 110)), std::invalid_argument);
+}
+
+TEST("layer: gradients follow the detached-norm contract (test_layer.cpp:174)") {
+    const DoraLinearState st = layer_state(8, 8, 6, 2);
+    const RealMatrix x = gaussian_fixture(3, 6, 0.0, 1.0, 109);
+    const LayerForwardResult f = layer_forward(st, x);
+    RealMatrix dy(3, 8, DTypeSpec::fp32());
+    for (double& v : dy.mutable_data()) v = 1.0;
+    const LayerGrads gr = layer_backward(st, f.saved, dy);
+    const std::vector<double> wn = f.saved.w_norm;
+    auto loss = [&](const AdapterPair& ad, const std::vector<double>& n) {
+        double acc = 0.0;
+        for (index_t i = 0; i < x.rows(); ++i)
+            for (index_t o = 0; o < st.d_out(); ++o) {
+                double base = 0.0, lora = 0.0;
+                for (index_t k = 0; k < st.d_in(); ++k) base += x(i, k) * st.w(o, k);
+                for (index_t l = 0; l < ad.rank(); ++l) {
+                    double mid = 0.0;
+                    for (index_t k = 0; k < st.d_in(); ++k) mid += x(i, k) * ad.A(l, k);
+                    lora += mid * ad.B(o, l);
+                }
+                const double g = st.magnitude.values[o] / std::max(n[o], 1e-12);
+                acc += g * base + g * (ad.s * lora) + (st.bias ? (*st.bias)[o] : 0.0);
+            }
+        return acc;
+    };
+    auto rel = [](double a, double b) { return std::fabs(a - b) / std::max(std::fabs(a) + std::fabs(b), 1e-6); };
+    double worst_det = 0.0, worst_inc = 0.0;
+    AdapterPair ad = st.adapter;
+    for (index_t l = 0; l < ad.rank(); ++l)
+        for (index_t k = 0; k < st.d_in(); ++k) {
+            const double th = ad.A(l, k), h = 1e-3 * std::max(1.0, std::fabs(th));
+            ad.A.set(l, k, th + h);
+            const double up_t = ad.A(l, k), up = loss(ad, wn), upf = loss(ad, dense_norm_f64(st.w, ad));
+            ad.A.set(l, k, th - h);
+            const double dn = loss(ad, wn), dnf = loss(ad, dense_norm_f64(st.w, ad));
+            const double den = up_t - ad.A(l, k);
+            ad.A.set(l, k, th);
+            worst_det = std::max(worst_det, rel(gr.d_a(l, k), (up - dn) / den));
+            worst_inc = std::max(worst_inc, rel(gr.d_a(l, k), (upf - dnf) / den));
+        }
+    std::printf("    detached %.2e, norm-attached %.2e\n", worst_det, worst_inc);
+    CHECK(worst_det <= 1e-3);
+    CHECK(worst_inc > 1e-2);
+}
+
+TEST("layer: bf16 forward + backward bitwise vs the host statement (layer.cpp:51-165)") {
+    const DTypeSpec& bf16 = DTypeSpec::bf16e();
+    for (const auto& shp : {std::array<index_t, 4>{33, 136, 200, 8}, std::array<index_t, 4>{64, 256, 128, 16}}) {
+        const index_t rows = shp[0], d_in = shp[1], d_out = shp[2], r = shp[3];
+        const DoraLinearState st = layer_state(31 + rows, d_out, d_in, r, true, bf16);
+        const RealMatrix x = gaussian_fixture(rows, d_in, 0.0, 1.0, 300 + rows, bf16);
+        const LayerForwardResult f = layer_forward(st, x);
+        const RealMatrix base = host_matmul(x, st.w, true, bf16);
+        const RealMatrix mid = host_matmul(x, st.adapter.A, true, bf16);
+        const RealMatrix lora = host_matmul(mid, st.adapter.B, true, bf16);
+        CHECK(same_bits(f.saved.base_out, base));
+        CHECK(same_bits(f.saved.lora_mid, mid));
+        CHECK(same_bits(f.saved.lora_out, lora));
+        const RealMatrix delta = host_stable(base, lora, f.saved.g, st.adapter.s, bf16);
+        bool y_ok = true;
+        for (index_t i = 0; i < rows; ++i)
+            for (index_t j = 0; j < d_out; ++j) {
+                double v = round_to_dtype(static_cast<float>(base(i, j)) + static_cast<float>(delta(i, j)), bf16);
+                v = round_to_dtype(static_cast<float>(v) + static_cast<float>((*st.bias)[j]), bf16);
+                y_ok &= f.y(i, j) == v;
+            }
+        CHECK(y_ok);
+        const RealMatrix dy = gaussian_fixture(rows, d_out, 0.0, 1.0, 400 + rows, bf16);
+        const LayerGrads gr = layer_backward(st, f.saved, dy);
+        const GradBundle gb = compose_backward(dy, f.saved.g, st.adapter.s, &*f.saved.inner,
+                                               f.saved.w_norm, true);
+        const RealMatrix d_b = host_matmul(host_transpose(gb.d_lora), mid, false, bf16);
+        const RealMatrix d_mid = host_matmul(gb.d_lora, st.adapter.B, false, bf16);
+        const RealMatrix d_a = host_matmul(host_transpose(d_mid), x, false, bf16);
+        CHECK(same_bits(gr.d_b, d_b));
+        CHECK(same_bits(gr.d_a, d_a));
+        CHECK(*gr.d_mag == *gb.d_mag);
+    }
 }
 
 // ------------------------------------------------------------------ acceptance.cpp

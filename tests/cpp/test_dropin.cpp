@@ -613,6 +613,31 @@ RealMatrix host_oracle_forward(const DoraLinearState& st, const RealMatrix& x) {
     return y;
 }
 
+// fp64 loss sum(y) with the norm held fixed at wn (the detached-norm gradient contract)
+double detached_loss(const DoraLinearState& st, const RealMatrix& x, const AdapterPair& ad,
+                     const Magnitude& m, const std::vector<double>& wn) {
+    double acc = 0.0;
+    for (index_t i = 0; i < x.rows(); ++i)
+        for (index_t o = 0; o < st.d_out(); ++o) {
+            double base = 0.0, lora = 0.0;
+            for (index_t k = 0; k < st.d_in(); ++k) base += x(i, k) * st.w(o, k);
+            for (index_t l = 0; l < ad.rank(); ++l) {
+                double mid = 0.0;
+                for (index_t k = 0; k < st.d_in(); ++k) mid += x(i, k) * ad.A(l, k);
+                lora += mid * ad.B(o, l);
+            }
+            const double g = m.values[o] / std::max(wn[o], 1e-12);
+            acc += g * base + g * (ad.s * lora) + (st.bias ? (*st.bias)[o] : 0.0);
+        }
+    return acc;
+}
+
+double fd_rel(double got, double want) {
+    return std::fabs(got - want) / std::max(std::fabs(got) + std::fabs(want), 1e-6);
+}
+
+double fd_h(double theta) { return 1e-3 * std::max(1.0, std::fabs(theta)); }
+
 }  // namespace
 
 TEST("layer: matmul_f32 is the serial fp32 product (matrix.cpp:53)") {
@@ -752,22 +777,9 @@ TEST("layer: gradients follow the detached-norm contract (test_layer.cpp:174)") 
     const LayerGrads gr = layer_backward(st, f.saved, dy);
     const std::vector<double> wn = f.saved.w_norm;
     auto loss = [&](const AdapterPair& ad, const std::vector<double>& n) {
-        double acc = 0.0;
-        for (index_t i = 0; i < x.rows(); ++i)
-            for (index_t o = 0; o < st.d_out(); ++o) {
-                double base = 0.0, lora = 0.0;
-                for (index_t k = 0; k < st.d_in(); ++k) base += x(i, k) * st.w(o, k);
-                for (index_t l = 0; l < ad.rank(); ++l) {
-                    double mid = 0.0;
-                    for (index_t k = 0; k < st.d_in(); ++k) mid += x(i, k) * ad.A(l, k);
-                    lora += mid * ad.B(o, l);
-                }
-                const double g = st.magnitude.values[o] / std::max(n[o], 1e-12);
-                acc += g * base + g * (ad.s * lora) + (st.bias ? (*st.bias)[o] : 0.0);
-            }
-        return acc;
+        return detached_loss(st, x, ad, st.magnitude, n);
     };
-    auto rel = [](double a, double b) { return std::fabs(a - b) / std::max(std::fabs(a) + std::fabs(b), 1e-6); };
+    auto rel = fd_rel;
     double worst_det = 0.0, worst_inc = 0.0;
     AdapterPair ad = st.adapter;
     for (index_t l = 0; l < ad.rank(); ++l)
@@ -844,6 +856,60 @@ TEST("acceptance criterion 4: 1000 ragged cases bitwise (acceptance.cpp:122)") {
     }
     std::printf("    %d/1000 bitwise identical\n", equal);
     CHECK(equal == 1000);
+}
+
+TEST("acceptance criterion 7: gradients vs finite differences, 20 instances (acceptance.cpp:198)") {
+    double worst = 0.0;
+    for (std::uint64_t inst = 0; inst < 20; ++inst) {
+        const std::uint64_t seed = derive_seed(88000, inst);
+        const index_t rows = 2 + seed % 4, d_in = 3 + derive_seed(seed, 1) % 6;
+        const index_t d_out = 3 + derive_seed(seed, 2) % 8, r = 1 + derive_seed(seed, 3) % 3;
+        RealMatrix w = gaussian_fixture(d_out, d_in, 0.0, 0.5, derive_seed(seed, 4));
+        AdapterPair a0{gaussian_fixture(r, d_in, 0.0, 0.5, derive_seed(seed, 5)),
+                       gaussian_fixture(d_out, r, 0.0, 0.5, derive_seed(seed, 6)),
+                       2.0 / std::sqrt(static_cast<double>(r))};
+        Magnitude mag{gaussian_vector(d_out, 1.5, 0.2, derive_seed(seed, 7)), DTypeSpec::fp32()};
+        const DoraLinearState st = make_layer_state(std::move(w), std::move(a0), std::move(mag),
+                                                    std::nullopt, DTypeSpec::fp32());
+        const RealMatrix x = gaussian_fixture(rows, d_in, 0.0, 1.0, derive_seed(seed, 8));
+        const LayerForwardResult f = layer_forward(st, x);
+        RealMatrix dy(rows, d_out, DTypeSpec::fp32());
+        for (double& v : dy.mutable_data()) v = 1.0;
+        const LayerGrads gr = layer_backward(st, f.saved, dy);
+        const std::vector<double>& wn = f.saved.w_norm;
+        AdapterPair ad = st.adapter;
+        // central differences on the stored (fp64) parameter, step as the reference takes it
+        auto fd = [&](RealMatrix& p, index_t i, index_t j) {
+            const double th = p(i, j), h = fd_h(th);
+            p.set(i, j, th + h);
+            const double up_t = p(i, j), up = detached_loss(st, x, ad, st.magnitude, wn);
+            p.set(i, j, th - h);
+            const double dn = detached_loss(st, x, ad, st.magnitude, wn), den = up_t - p(i, j);
+            p.set(i, j, th);
+            return (up - dn) / den;
+        };
+        for (index_t l = 0; l < r; ++l)
+            for (index_t k = 0; k < d_in; ++k) worst = std::max(worst, fd_rel(gr.d_a(l, k), fd(ad.A, l, k)));
+        for (index_t o = 0; o < d_out; ++o)
+            for (index_t l = 0; l < r; ++l) worst = std::max(worst, fd_rel(gr.d_b(o, l), fd(ad.B, o, l)));
+        Magnitude m = st.magnitude;
+        for (index_t o = 0; o < d_out; ++o) {
+            const double th = m.values[o], h = fd_h(th);
+            m.values[o] = round_to_dtype(th + h, DTypeSpec::fp32());
+            const double up_t = m.values[o], up = detached_loss(st, x, st.adapter, m, wn);
+            m.values[o] = round_to_dtype(th - h, DTypeSpec::fp32());
+            const double dn = detached_loss(st, x, st.adapter, m, wn), den = up_t - m.values[o];
+            m.values[o] = th;
+            worst = std::max(worst, fd_rel((*gr.d_mag)[o], (up - dn) / den));
+        }
+    }
+    const GradBundle z = compose_backward(gaussian_fixture(16, 48, 0.0, 1.0, 91011),
+                                          std::vector<double>(48, 1.0), 0.7, nullptr, {}, false);
+    bool d_base_zero = true;
+    for (double v : z.d_base.data()) d_base_zero &= v == 0.0;
+    std::printf("    20 instances, max rel err %.2e vs 1e-3\n", worst);
+    CHECK(worst <= 1e-3);
+    CHECK(d_base_zero);
 }
 
 int main(int argc, char** argv) { return mini::run_all(argc > 1 ? argv[1] : nullptr); }

@@ -587,11 +587,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int k = 0; k < kBK / 16; ++k) {
                             const uint64_t ad = umma_desc_k_sw128(sx + k * 32);
                             const uint64_t bd = umma_desc_k_sw128(sy + k * 32);
+#ifndef DFX_KO_MMA
                             umma_f16_pair(tacc + static_cast<uint32_t>(h * p.bn), ad, bd, idesc,
                                           (it > 0 || k > 0) ? 1u : 0u);
+#else
+                            (void)ad; (void)bd;
+#endif
                         }
                     }
+#ifndef DFX_KO_COMMIT
                     umma_commit_pair_mc(&empty[s], 0x3);
+#else
+                    mbar_arrive(&empty[s]);
+                    mbar_arrive_remote(mapa_shared(smem_u32(&empty[s]), 1), 1);
+#endif
                     if (++s == p.stages) { s = 0; ph ^= 1; }
                 }
                 umma_commit_pair_mc(&tmem_full[slot], 0x3);
@@ -644,6 +653,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t trow = tmem_base + static_cast<uint32_t>(slot) * slot_cols +
                                   (static_cast<uint32_t>(q * 32) << 16);
             float acc = 0.0f;
+#ifdef DFX_KO_EPI
+            if (bn_pair < 0)
+#endif
             for (int c0 = 0; c0 < bn_pair; c0 += 32) {
                 uint32_t u[32];
                 tmem_ld_32x32b_x32(trow + c0, u);
@@ -1063,6 +1075,9 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         p.x_kwrap = 0; p.chunk = a.chunk_size;
         p.Z = static_cast<const __nv_bfloat16*>(a.b); p.ldz = r;
         p.out = cross; p.base_out = base; p.do_chain = 1;
+#ifdef DFX_KO_CHAIN
+        p.do_chain = 0;
+#endif
         if (u.pair) {
             // A box = half of the pair's BN rows (each CTA of the pair loads its half)
             e = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, u.sp.bn / 2, true);
@@ -1071,6 +1086,10 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
             p.stages = stages_for_pair(u.sp.bn, u.nh);
             p.tiles = static_cast<int>(pm_tiles * u.sp.ns);
             const int pairs = std::min<int>(p.tiles, std::max(1, u.ctas / (2 * u.ks)));
+            if (std::getenv("DFX_PLAN_PRINT"))
+                std::fprintf(stderr, "u plan: pairs %d ks %d kbps %d tiles %d n_split %d bn %d nh %d stages %d"
+                             " strategy %d side %d sms %d\n", pairs, u.ks, u.kbps, p.tiles, p.n_split, p.bn,
+                             p.nh, p.stages, int(plan.strategy), plan.side, sms);
             e = launch_tc_pair(tw, ta, p, pairs, u.ks, st, "u_rowdot_tc");
         } else {
             e = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, u.sp.bn, true);

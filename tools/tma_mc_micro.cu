@@ -34,7 +34,7 @@ __device__ __forceinline__ void bulk_load_mc(void* dst, const void* src, uint32_
 
 template <int C>
 __global__ void __launch_bounds__(64) stream_kernel(const char* __restrict__ w, const char* __restrict__ a,
-                                                    uint32_t kA, int iters, long long* cycles) {
+                                                    uint32_t kA, int iters, long long* cycles, size_t wrap) {
     extern __shared__ __align__(1024) char smem[];
     __shared__ uint64_t full[kStages], empty[kStages];
     const uint32_t stage_bytes = kW + kA;
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(64) stream_kernel(const char* __restrict__ w, 
             if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
             char* dst = smem + s * stage_bytes;
             mbar_arrive_expect_tx(&full[s], stage_bytes);
-            bulk_load(dst, w + (static_cast<size_t>(blockIdx.x) * iters + it) * kW, kW, &full[s]);
+            bulk_load(dst, w + ((static_cast<size_t>(blockIdx.x) * iters + it) % wrap) * kW, kW, &full[s]);
             const char* asrc = a + static_cast<size_t>(it % 64) * kA;
             if (C == 1) {
                 bulk_load(dst + kW, asrc, kA, &full[s]);
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(64) stream_kernel(const char* __restrict__ w, 
 }
 
 template <int C>
-void run(const char* w, const char* a, uint32_t kA, int iters, long long* cyc, int sms) {
+void run(const char* w, const char* a, uint32_t kA, int iters, long long* cyc, int sms, size_t wrap) {
     const int grid = (sms / C) * C;
     const size_t smem = kStages * (kW + kA);
     cudaFuncSetAttribute(stream_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -103,7 +103,7 @@ void run(const char* w, const char* a, uint32_t kA, int iters, long long* cyc, i
     cudaEventCreate(&e1);
     for (int rep = 0; rep < 3; ++rep) {
         cudaEventRecord(e0);
-        cudaError_t err = cudaLaunchKernelEx(&cfg, stream_kernel<C>, w, a, kA, iters, cyc);
+        cudaError_t err = cudaLaunchKernelEx(&cfg, stream_kernel<C>, w, a, kA, iters, cyc, wrap);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         if (err != cudaSuccess || cudaGetLastError() != cudaSuccess) {
@@ -116,8 +116,8 @@ void run(const char* w, const char* a, uint32_t kA, int iters, long long* cyc, i
         cudaMemcpy(h, cyc, sizeof(long long), cudaMemcpyDeviceToHost);
         const double per_sm = double(kW + kA) * iters / double(h[0]);
         if (rep == 2)
-            std::printf("C=%d grid=%d kA=%u: %.1f us, %.1f B/clk/SM delivered (W+A), chip %.2f TB/s delivered\n",
-                        C, grid, kA, ms * 1e3, per_sm, double(kW + kA) * iters * grid / (ms * 1e-3) / 1e12);
+            std::printf("wrap=%zu C=%d grid=%d kA=%u: %.1f us, %.1f B/clk/SM delivered (W+A), chip %.2f TB/s delivered\n",
+                        wrap, C, grid, kA, ms * 1e3, per_sm, double(kW + kA) * iters * grid / (ms * 1e-3) / 1e12);
     }
 }
 
@@ -132,13 +132,16 @@ int main() {
     cudaMalloc(&cyc, sizeof(long long) * sms);
     cudaMemset(w, 1, size_t(sms) * iters * kW);
     cudaMemset(a, 2, size_t(64) * 32768);
-    for (uint32_t kA : {12288u, 24576u}) {
-        run<1>(w, a, kA, iters, cyc, sms);
-        run<2>(w, a, kA, iters, cyc, sms);
-        run<4>(w, a, kA, iters, cyc, sms);
-        run<8>(w, a, kA, iters, cyc, sms);
+    for (size_t wrap : {size_t(sms) * iters, size_t(2048)}) {   // W from HBM / W L2-resident
+        for (uint32_t kA : {12288u, 24576u}) {
+            run<1>(w, a, kA, iters, cyc, sms, wrap);
+            run<2>(w, a, kA, iters, cyc, sms, wrap);
+            run<4>(w, a, kA, iters, cyc, sms, wrap);
+            run<8>(w, a, kA, iters, cyc, sms, wrap);
+        }
+        run<1>(w, a, 12288u, iters, cyc, 64, wrap);
+        run<4>(w, a, 12288u, iters, cyc, 64, wrap);
+        run<8>(w, a, 12288u, iters, cyc, 64, wrap);
     }
-    run<1>(w, a, 12288u, iters, cyc, 64);
-    run<4>(w, a, 12288u, iters, cyc, 64);
     return 0;
 }

@@ -438,6 +438,34 @@ def run_gpu(args, rank, world, local_rank, dist):
             "unfused": "cuBLAS bf16 GEMM -> lora (HBM), dfx_compose_fwd dual, torch.add residual"}
         log(f"lora_compose fused {tf:.1f} us vs unfused {tu:.1f} us")
 
+        # ---- cached ||W||^2_row of a frozen W; W is still read
+        # for the cross term, the base_sq chain is skipped.  Full GPU, rotating buffer sets.
+        dfx.set_sm_budget(0)
+        caches = [torch.empty(d_out, device=dev) for _ in sets]
+        for c, bb in zip(caches, sets):
+            dfx.row_norm_cached(bb["W"], bb["A"], bb["B"], s, cs, c, bb["wn"], refresh=True,
+                                m=bb["m"], g=bb["g"])
+        it = {"k": 0}
+
+        def norm_plain():
+            bb = sets[it["k"] % len(sets)]
+            it["k"] += 1
+            dfx.row_norm(bb["W"], bb["A"], bb["B"], s, cs, bb["wn"], m=bb["m"], g=bb["g"])
+
+        def norm_cached():
+            k = it["k"] % len(sets)
+            it["k"] += 1
+            bb = sets[k]
+            dfx.row_norm_cached(bb["W"], bb["A"], bb["B"], s, cs, caches[k], bb["wn"], m=bb["m"],
+                                g=bb["g"])
+
+        tn, tc = batch_time(norm_plain, args.lora_steps), batch_time(norm_cached, args.lora_steps)
+        variants["norm_cached_base_sq"] = {
+            "what": "row_norm with ||W||^2_row cached for a frozen W (opt-in, departs from the "
+                    "reference's recompute-every-call contract; bitwise equal while W is unchanged)",
+            "plain_us": round(tn, 2), "cached_us": round(tc, 2), "speedup": round(tn / tc, 3)}
+        log(f"row_norm plain {tn:.1f} us vs cached base_sq {tc:.1f} us")
+
     # ---- per-kernel live durations (event-bracketed launches, same kernels/buffers)
     prof_steps = min(args.steps, args.prof_steps)
     set_budget(args.mode)

@@ -110,6 +110,19 @@ int dfx_row_norm(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A, co
                  const float* m, dfx_dtype mag_dtype, float* w_norm, float* g, float* terms,
                  dfx_stream_t stream);
 
+/* SURVEY 8(f) row 4, opt-in: the factored norm with a cached ||W||^2_row for a FROZEN W.
+ * refresh != 0: the full dfx_row_norm, which also writes base_sq [d_out] (fp32, the serial
+ * chain's value) into base_sq_cache.  refresh == 0: the W.A^T kernel runs without its
+ * base_sq chain and the finisher reads base_sq_cache instead; the result is bitwise the
+ * full call's as long as W is unchanged since the refresh.  This departs from the
+ * reference's contract, which recomputes the norm from W on every call
+ * (factored_norm.cpp:52-61) — the caller owns the cache's validity.  W is still read (the
+ * cross term needs W.A^T).  bf16 tensor-core shapes only (DFX_EUNSUPPORTED otherwise). */
+int dfx_row_norm_cached(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A,
+                        const void* B, int64_t d_out, int64_t d_in, int64_t r, double s,
+                        int64_t chunk_size, float* base_sq_cache, int refresh, const float* m,
+                        dfx_dtype mag_dtype, float* w_norm, float* g, dfx_stream_t stream);
+
 /* d_in-split (FSDP2-style) factored norm — the exchange the paper leaves open
  * (PAPER.md:1073-1078).  Step 1 on every rank: the terms of this rank's K slice,
  * W_k [d_out x d_in_k], A_k [r x d_in_k], full B [d_out x r]:

@@ -67,6 +67,8 @@ SIGNATURES = {
     "dfx_magnitude_scale": (_int, [_vp, _int, _vp, _vp, _i64, _vp, _vp]),
     "dfx_row_norm": (_int, [_vp, _int, _vp, _vp, _vp, _i64, _i64, _i64, _f64, _i64, _vp, _int,
                             _vp, _vp, _vp, _vp]),
+    "dfx_row_norm_cached": (_int, [_vp, _int, _vp, _vp, _vp, _i64, _i64, _i64, _f64, _i64, _vp,
+                                   _int, _vp, _int, _vp, _vp, _vp]),
     "dfx_norm_partial": (_int, [_vp, _int, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
                                 _vp]),
     "dfx_norm_finish": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _i64, _i64, _f64, _vp, _int, _vp, _vp,
@@ -176,6 +178,17 @@ class Dfx:
                                           float(s), int(chunk_size), _ptr(m),
                                           dt if mag_dtype is None else mag_dtype, _ptr(w_norm),
                                           _ptr(g), _ptr(terms), _stream(stream)))
+
+    def row_norm_cached(self, W, A, B, s, chunk_size, base_sq_cache, w_norm, refresh=False,
+                        m=None, g=None, mag_dtype=None, stream=None):
+        """Opt-in cached ||W||^2_row for a frozen W (dfx_row_norm_cached)."""
+        d_out, d_in = W.shape
+        r = A.shape[0]
+        dt = _dtype_code(W)
+        self._check(self.lib.dfx_row_norm_cached(
+            self.ctx, dt, _ptr(W), _ptr(A), _ptr(B), d_out, d_in, r, float(s), int(chunk_size),
+            _ptr(base_sq_cache), 1 if refresh else 0, _ptr(m),
+            dt if mag_dtype is None else mag_dtype, _ptr(w_norm), _ptr(g), _stream(stream)))
 
     def norm_partial(self, W_k, A_k, B, chunk_size, gram, base_sq, cross, stream=None):
         """d_in-split step 1: this rank's K-slice terms (sum them over ranks)."""

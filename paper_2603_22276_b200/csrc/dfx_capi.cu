@@ -431,6 +431,35 @@ int dfx_row_norm(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A, co
                     w_norm, g, dtype, stream, "dfx_row_norm");
 }
 
+int dfx_row_norm_cached(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A,
+                        const void* B, int64_t d_out, int64_t d_in, int64_t r, double s,
+                        int64_t chunk_size, float* base_sq_cache, int refresh, const float* m,
+                        dfx_dtype mag_dtype, float* w_norm, float* g, dfx_stream_t stream) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    rc = check_norm_args(dtype, W, A, B, d_out, d_in, r, chunk_size);
+    if (rc) return rc;
+    if (!base_sq_cache && d_out > 0) return fail(DFX_EINVAL, "dfx_row_norm_cached: null cache");
+    if (m && !valid_dtype(mag_dtype)) return fail(DFX_EUNSUPPORTED, "dfx_row_norm_cached: mag dtype");
+    if (m && !g) return fail(DFX_EINVAL, "dfx_row_norm_cached: m given without g output");
+    if (dtype == DFX_F32 || s == 0.0 || chunk_size % 64 != 0 ||
+        !dfx::norm_uses_tensor_cores(dtype, d_out, d_in, r))
+        return fail(DFX_EUNSUPPORTED, "dfx_row_norm_cached: needs the bf16 tensor-core path");
+    if (refresh)
+        return run_norm(ctx, dtype, W, A, B, d_out, d_in, r, s, chunk_size, base_sq_cache, nullptr,
+                        nullptr, m, mag_dtype, w_norm, g, dtype, stream, "dfx_row_norm_cached");
+    dfx::NormArgs a{};
+    a.dt = dtype; a.w = W; a.a = A; a.b = B;
+    a.d_out = d_out; a.d_in = d_in; a.r = r; a.s = s; a.chunk_size = chunk_size;
+    a.m = m; a.w_norm = w_norm; a.g = g;
+    a.round_dt = dtype; a.mag_dt = mag_dtype;
+    a.base_cached = base_sq_cache;
+    int launches = 0;
+    const cudaError_t e = dfx::launch_norm(a, &ctx->ws, stream, &launches);
+    ctx->launches += launches;
+    return finish_call(e, "dfx_row_norm_cached");
+}
+
 int dfx_norm_partial(dfx_ctx* ctx, dfx_dtype dtype, const void* W_k, const void* A_k,
                      const void* B, int64_t d_out, int64_t d_in_k, int64_t r, int64_t chunk_size,
                      float* gram, float* base_sq, float* cross, dfx_stream_t stream) {

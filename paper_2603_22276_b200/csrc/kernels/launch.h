@@ -75,6 +75,10 @@ struct NormArgs {
     const float* gram_in;   // finish: reduced fp32 Gram [r x r]
     const float* base_in;   // finish: reduced base_sq [d_out]
     const float* cross_in;  // finish: reduced cross [d_out]
+    // full mode with a cached base_sq [d_out] of a frozen W (from an
+    // earlier call's base_sq output): the U kernel runs without its base_sq chain and the
+    // finisher takes the cached value.  bf16 tensor-core path only.
+    const float* base_cached;
 };
 
 enum NormMode : int { kNormFull = 0, kNormPartial = 1, kNormFinish = 2 };

@@ -332,9 +332,12 @@ cudaError_t launch_norm(const NormArgs& a, Workspace* ws, cudaStream_t st, int* 
     if (a.d_out == 0) return cudaSuccess;
     // the tensor-core chain walks 64-wide K blocks: chunk boundaries must align to them
     const int64_t tc_din = a.mode == kNormFinish ? 64 : a.d_in;  // finish reads no W
-    if ((a.s != 0.0 || a.mode == kNormPartial) && a.chunk_size % 64 == 0 &&
-        norm_tc_supported(a.dt, a.d_out, tc_din, a.r))
+    const bool tc = a.chunk_size % 64 == 0 && norm_tc_supported(a.dt, a.d_out, tc_din, a.r);
+    if (a.base_cached) {   // only the tensor-core U kernel can drop its chain
+        if (a.mode != kNormFull || !tc || a.s == 0.0) return cudaErrorNotSupported;
         return launch_norm_tc(a, ws, st, launches);
+    }
+    if ((a.s != 0.0 || a.mode == kNormPartial) && tc) return launch_norm_tc(a, ws, st, launches);
     if (a.dt == kF32 && a.s != 0.0 && a.mode == kNormFull && norm_tf32_enabled() &&
         norm_tc_f32_supported(a.d_out, a.d_in, a.r, a.chunk_size))
         return launch_norm_tc_f32(a, ws, st, launches);

@@ -1075,6 +1075,7 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         p.x_kwrap = 0; p.chunk = a.chunk_size;
         p.Z = static_cast<const __nv_bfloat16*>(a.b); p.ldz = r;
         p.out = cross; p.base_out = base; p.do_chain = 1;
+        if (a.base_cached) p.do_chain = 0;     // frozen W: base_sq comes from the cache
 #ifdef DFX_KO_CHAIN
         p.do_chain = 0;
 #endif
@@ -1159,6 +1160,7 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
 
     FinishArgs f{};
     f.base_part = base; f.base_parts = static_cast<int>(n_chunks);
+    if (a.base_cached) { f.base_part = a.base_cached; f.base_parts = 1; }
     f.cross_part = cross; f.cross_parts = u.ks * u.sp.ns;
     if (!partial) { f.ba_part = ba; f.ba_parts = plan.sb.ns; }
     f.d_out = d_out; f.two_s = 2.0 * a.s; f.s2 = a.s * a.s;

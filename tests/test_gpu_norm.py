@@ -322,3 +322,68 @@ def test_fp32_c1_full_size(dfx, oracle):
     f64 = oracle.dense_row_norm_f64(Ws, A, Bs, s)
     kappa = _kappa(oracle, Ws, A, Bs, s)
     assert np.all(np.abs(wn[rows] - f64) <= np.maximum(1e-5, 64 * kappa * 2.0 ** -24) * f64)
+
+
+@pytest.mark.parametrize("budget", [0, 80])
+@pytest.mark.parametrize("d_out,d_in,r,dt", [(1024, 1024, 384, 1), (2048, 4096, 64, 1),
+                                             (768, 4608, 320, 1), (8192, 8192, 384, 1)])
+def test_row_norm_cached(oracle, budget, d_out, d_in, r, dt):
+    """the cached ||W||^2_row of a frozen W.  The refresh call is
+    the full norm and fills the cache with base_sq (bitwise the serial chain); the cached call
+    runs W.A^T without the chain and gives bitwise the full call's w_norm and g while W is
+    unchanged — with a new A and B too (the trainable factors move every step).  A W edited
+    after the refresh is the caller's responsibility: the cached call then differs."""
+    import torch
+    import paper_2603_22276_b200 as P
+    dfx = P.Dfx(0)
+    dfx.set_sm_budget(budget)
+    tdt = torch.bfloat16 if dt == 1 else torch.float16
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(d_out + r + budget)
+    W = torch.randn(d_out, d_in, device="cuda", generator=gen).to(tdt)
+    cs, _ = oracle.plan_chunks(d_out, d_in)
+    s = 2.0 / np.sqrt(r)
+    m = torch.rand(d_out, device="cuda", generator=gen) * 50 + 10
+    cache = torch.full((d_out,), float("nan"), device="cuda")
+    for step in range(2):
+        A = (0.05 * torch.randn(r, d_in, device="cuda", generator=gen)).to(tdt)
+        B = (0.05 * torch.randn(d_out, r, device="cuda", generator=gen)).to(tdt)
+        wn0, g0 = torch.empty(d_out, device="cuda"), torch.empty(d_out, device="cuda")
+        terms = torch.empty(3, d_out, device="cuda")
+        dfx.row_norm(W, A, B, s, cs, wn0, m=m, g=g0, terms=terms)
+        wn1, g1 = torch.empty_like(wn0), torch.empty_like(g0)
+        if step == 0:
+            dfx.row_norm_cached(W, A, B, s, cs, cache, wn1, refresh=True, m=m, g=g1)
+            torch.cuda.synchronize()
+            assert bits_equal(to_np(cache), to_np(terms[0]))
+        else:
+            dfx.row_norm_cached(W, A, B, s, cs, cache, wn1, m=m, g=g1)
+        torch.cuda.synchronize()
+        assert bits_equal(to_np(wn1), to_np(wn0)), f"step {step}"
+        assert bits_equal(to_np(g1), to_np(g0)), f"step {step}"
+    W[0].mul_(2)
+    fresh = torch.empty(d_out, device="cuda")
+    dfx.row_norm(W, A, B, s, cs, fresh)
+    stale = torch.empty(d_out, device="cuda")
+    dfx.row_norm_cached(W, A, B, s, cs, cache, stale)
+    torch.cuda.synchronize()
+    assert to_np(stale)[0] != to_np(fresh)[0]
+    assert bits_equal(to_np(stale)[1:], to_np(fresh)[1:])
+    dfx.close()
+
+
+def test_row_norm_cached_rejects(dfx):
+    import torch
+    import paper_2603_22276_b200 as P
+    W = torch.zeros(256, 512, device="cuda")
+    A, B = torch.zeros(16, 512, device="cuda"), torch.zeros(256, 16, device="cuda")
+    c, wn = torch.zeros(256, device="cuda"), torch.zeros(256, device="cuda")
+    with pytest.raises(P.DfxError):      # fp32: not the bf16/fp16 tensor-core path
+        dfx.row_norm_cached(W, A, B, 0.5, 512, c, wn)
+    Wb, Ab, Bb = W.bfloat16(), A.bfloat16(), B.bfloat16()
+    with pytest.raises(P.DfxError):      # fp16: the norm's tensor-core kernels are bf16
+        dfx.row_norm_cached(W.half(), A.half(), B.half(), 0.5, 512, c, wn)
+    with pytest.raises(P.DfxError):      # s == 0 has no cross term to compute
+        dfx.row_norm_cached(Wb, Ab, Bb, 0.0, 512, c, wn)
+    with pytest.raises(P.DfxInvalidArgument):
+        dfx.row_norm_cached(Wb, Ab, Bb, 0.5, 512, None, wn)   # no cache buffer

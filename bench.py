@@ -286,8 +286,10 @@ def run_gpu(args, rank, world, local_rank, dist):
                             d_mag=b["dm"], stream=st)
 
     def step(b, mode):
-        norm(b)
-        compose(b, mode)
+        if args.only != "compose":
+            norm(b)
+        if args.only != "norm":
+            compose(b, mode)
 
     stream = torch.cuda.Stream(device=dev)
     side = torch.cuda.Stream(device=dev)
@@ -315,10 +317,12 @@ def run_gpu(args, rank, world, local_rank, dist):
                     b = sets[i % nbuf]
                     if i >= nbuf:
                         stream.wait_event(ev_comp[i - nbuf])
-                    norm(b, sA)
+                    if args.only != "compose":
+                        norm(b, sA)
                     ev_norm[i].record(stream)
                     side.wait_event(ev_norm[i])
-                    compose(b, mode, sB)
+                    if args.only != "norm":
+                        compose(b, mode, sB)
                     ev_comp[i].record(side)
                 stream.wait_event(ev_comp[npipe - 1])
             graphs.append(gph)
@@ -382,6 +386,12 @@ def run_gpu(args, rank, world, local_rank, dist):
     ms, npipe = timed(args.mode, args.steps, args.warmup, clk)
     value = world * args.steps / (ms / 1e3)
     log(f"timed ({args.mode}): {args.steps} steps in {ms:.3f} ms -> {value:.1f} modules/s")
+    if args.only:   # stage analysis: not a bench line
+        if rank == 0:
+            print(json.dumps({"only": args.only, "value": round(value, 3),
+                              "ms_per_step": round(ms / args.steps, 5),
+                              "norm_sm_budget": args.norm_sms}), flush=True)
+        return
 
     # ---- the other variant (inference module / training step), same protocol
     variants = {}
@@ -817,6 +827,8 @@ def main():
     ap.add_argument("--impl", default="dfx", choices=["dfx", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c5"])
     ap.add_argument("--nbuf", type=int, default=4)
+    ap.add_argument("--only", default="", choices=["", "norm", "compose"],
+                    help="analysis: time one stage of the step alone (not a bench number)")
     ap.add_argument("--prof-steps", type=int, default=40)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")

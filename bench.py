@@ -527,6 +527,19 @@ def run_gpu(args, rank, world, local_rank, dist):
                 "peak_source": f"{peak_src}: bf16 sustained {peak_tf_sus} TF/s (burst "
                                f"{peak_tf_burst}), HBM copy {peaks_hbm} GB/s",
                 "avg_us": dk["avg_us"], "share": dk["share"]}
+    if dom == "u_rowdot_tc" and cfg["dtype"] == "bf16":
+        # the SMs this launch occupies under the step's SM budget (the others run the composes):
+        # the same achieved rate against the sustained peak scaled to those SMs
+        try:
+            u_sms, side_sms, strat = dfx.norm_plan(d_out, d_in, r, cs)
+            nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+            roofline["sms_used"] = u_sms
+            roofline["frac_of_sms_used"] = round(dk["achieved"] / (peak_tf_sus * u_sms / nsm), 4)
+            roofline["norm_plan"] = {"u_sms": u_sms, "side_sms": side_sms,
+                                     "strategy": ["gram+V beside U", "gram beside, V after",
+                                                  "serial"][strat]}
+        except Exception as ex:  # noqa: BLE001 - context only, never fails the bench
+            log(f"norm_plan unavailable: {ex}")
     if args.pipeline > 1 and args.norm_sms > 0:
         # the same W.A^T GEMM planned for the whole GPU (no SM budget), timed alone
         dfx.set_sm_budget(0)

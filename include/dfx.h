@@ -198,6 +198,13 @@ int dfx_module_train_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const vo
                           int64_t rows, int64_t chunk_size, void* delta, void* d_lora,
                           void* d_base, float* d_mag, float* g);
 
+/* The bf16 tensor-core norm's plan for this shape under the context's SM budget
+ * (dfx_ctx_set_sm_budget): SMs the W.A^T kernel occupies, SMs given to the Gram / V
+ * kernels on the side stream (0 when they run after it), strategy (0 Gram and V beside
+ * W.A^T, 1 Gram beside and V after, 2 serial).  DFX_EUNSUPPORTED off the tensor-core path. */
+int dfx_norm_plan(dfx_ctx* ctx, dfx_dtype dtype, int64_t d_out, int64_t d_in, int64_t r,
+                  int64_t chunk_size, int* u_sms, int* side_sms, int* strategy);
+
 /* 1 when dfx_row_norm takes the tcgen05/TMA path for this (dtype, shape). */
 int dfx_norm_uses_tensor_cores(dfx_dtype dtype, int64_t d_out, int64_t d_in, int64_t r);
 

@@ -67,6 +67,7 @@ SIGNATURES = {
     "dfx_magnitude_scale": (_int, [_vp, _int, _vp, _vp, _i64, _vp, _vp]),
     "dfx_row_norm": (_int, [_vp, _int, _vp, _vp, _vp, _i64, _i64, _i64, _f64, _i64, _vp, _int,
                             _vp, _vp, _vp, _vp]),
+    "dfx_norm_plan": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _vp, _vp, _vp]),
     "dfx_row_norm_cached": (_int, [_vp, _int, _vp, _vp, _vp, _i64, _i64, _i64, _f64, _i64, _vp,
                                    _int, _vp, _int, _vp, _vp, _vp]),
     "dfx_norm_partial": (_int, [_vp, _int, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
@@ -178,6 +179,13 @@ class Dfx:
                                           float(s), int(chunk_size), _ptr(m),
                                           dt if mag_dtype is None else mag_dtype, _ptr(w_norm),
                                           _ptr(g), _ptr(terms), _stream(stream)))
+
+    def norm_plan(self, d_out, d_in, r, chunk_size, dtype=BF16):
+        """(u_sms, side_sms, strategy) of the tensor-core norm under the current SM budget."""
+        u, sd, st = C.c_int(), C.c_int(), C.c_int()
+        self._check(self.lib.dfx_norm_plan(self.ctx, dtype, d_out, d_in, r, int(chunk_size),
+                                           C.byref(u), C.byref(sd), C.byref(st)))
+        return u.value, sd.value, st.value
 
     def row_norm_cached(self, W, A, B, s, chunk_size, base_sq_cache, w_norm, refresh=False,
                         m=None, g=None, mag_dtype=None, stream=None):

@@ -369,6 +369,18 @@ int dfx_plan_chunks(uint64_t d_out, uint64_t d_in, uint64_t budget, uint64_t* ch
     return DFX_OK;
 }
 
+int dfx_norm_plan(dfx_ctx* ctx, dfx_dtype dtype, int64_t d_out, int64_t d_in, int64_t r,
+                  int64_t chunk_size, int* u_sms, int* side_sms, int* strategy) {
+    int rc = enter(ctx);
+    if (rc) return rc;
+    if (dtype != DFX_BF16 || chunk_size <= 0 || chunk_size % 64 != 0 ||
+        !dfx::norm_uses_tensor_cores(dtype, d_out, d_in, r))
+        return fail(DFX_EUNSUPPORTED, "dfx_norm_plan: not the bf16 tensor-core path");
+    dfx::norm_plan_info(d_out, d_in, r, chunk_size, dfx::ws_sm_count(&ctx->ws), u_sms, side_sms,
+                        strategy);
+    return DFX_OK;
+}
+
 int dfx_norm_uses_tensor_cores(dfx_dtype dtype, int64_t d_out, int64_t d_in, int64_t r) {
     return dfx::norm_uses_tensor_cores(dtype, d_out, d_in, r);
 }

@@ -109,5 +109,7 @@ cudaError_t launch_magnitude_scale(int dt, const float* m, const float* w_norm, 
 
 // Chooses the tensor-core path for (dt, shape); exposed for tests/bench reporting.
 int norm_uses_tensor_cores(int dt, int64_t d_out, int64_t d_in, int64_t r);
+void norm_plan_info(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, int sms,
+                    int* u_ctas, int* side_ctas, int* strategy);
 
 }  // namespace dfx

@@ -1017,6 +1017,27 @@ NormPlan plan_norm(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, i
     return best;
 }
 
+// The planner's decision for (shape, SM budget), for callers sizing what runs beside the norm
+// and for the bench's roofline context: SMs the W.A^T kernel occupies, SMs of the side
+// stream (Gram / V beside it; 0 when serial), the strategy (0 side-all, 1 side-gram, 2 serial).
+void norm_plan_info(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, int sms,
+                    int* u_ctas, int* side_ctas, int* strategy) {
+    const NormPlan plan = plan_norm(d_out, d_in, r, chunk_size, sms, true);
+    const UPlan& u = plan.u;
+    const int64_t pm_tiles = (d_out + 2 * kBM - 1) / (2 * kBM);
+    const int64_t m_tiles = (d_out + kBM - 1) / kBM;
+    int ctas;
+    if (u.pair) {
+        const int pairs = static_cast<int>(std::min<int64_t>(pm_tiles * u.sp.ns, std::max(1, u.ctas / (2 * u.ks))));
+        ctas = 2 * pairs * u.ks;
+    } else {
+        ctas = static_cast<int>(std::min<int64_t>(m_tiles * u.sp.ns, std::max(1, u.ctas / u.ks))) * u.ks;
+    }
+    if (u_ctas) *u_ctas = std::min(ctas, sms);
+    if (side_ctas) *side_ctas = plan.strategy == kSerial ? 0 : plan.side;
+    if (strategy) *strategy = static_cast<int>(plan.strategy);
+}
+
 cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, int* launches) {
     if (a.mode == kNormFinish) return launch_norm_finish_tc(a, ws, st, launches);
     if (!norm_tc_supported(a.dt, a.d_out, a.d_in, a.r)) return cudaErrorNotSupported;

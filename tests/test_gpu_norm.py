@@ -387,3 +387,18 @@ def test_row_norm_cached_rejects(dfx):
         dfx.row_norm_cached(Wb, Ab, Bb, 0.0, 512, c, wn)
     with pytest.raises(P.DfxInvalidArgument):
         dfx.row_norm_cached(Wb, Ab, Bb, 0.5, 512, None, wn)   # no cache buffer
+
+
+def test_norm_plan_reports_budget():
+    """dfx_norm_plan reports the planner's SM split; it follows dfx_ctx_set_sm_budget."""
+    import paper_2603_22276_b200 as P
+    dfx = P.Dfx(0)
+    u_all, _, _ = dfx.norm_plan(8192, 8192, 384, 8192)
+    for budget in (96, 80, 64, 24):
+        dfx.set_sm_budget(budget)
+        u, side, strat = dfx.norm_plan(8192, 8192, 384, 8192)
+        assert 0 < u <= budget and u + side <= budget and strat in (0, 1, 2)
+        assert u <= u_all
+    with pytest.raises(P.DfxError):
+        dfx.norm_plan(8192, 8192, 384, 8192, dtype=P.F32)
+    dfx.close()

@@ -281,9 +281,11 @@ def run_gpu(args, rank, world, local_rank, dist):
         if mode == "infer":
             dfx.compose_fwd(b["base"], b["lora"], b["g"], s, b["delta"], stream=st)
         else:
-            dfx.compose_fwd(b["base"], b["lora"], b["g"], s, b["delta"], b["inner"], stream=st)
-            dfx.compose_bwd(b["dy"], b["g"], s, b["dl"], b["db"], inner=b["inner"], w_norm=b["wn"],
-                            d_mag=b["dm"], stream=st)
+            if args.compose_parts != "bwd":
+                dfx.compose_fwd(b["base"], b["lora"], b["g"], s, b["delta"], b["inner"], stream=st)
+            if args.compose_parts != "fwd":
+                dfx.compose_bwd(b["dy"], b["g"], s, b["dl"], b["db"], inner=b["inner"],
+                                w_norm=b["wn"], d_mag=b["dm"], stream=st)
 
     def step(b, mode):
         if args.only != "compose":
@@ -386,9 +388,10 @@ def run_gpu(args, rank, world, local_rank, dist):
     ms, npipe = timed(args.mode, args.steps, args.warmup, clk)
     value = world * args.steps / (ms / 1e3)
     log(f"timed ({args.mode}): {args.steps} steps in {ms:.3f} ms -> {value:.1f} modules/s")
-    if args.only:   # stage analysis: not a bench line
+    if args.only or args.compose_parts != "both":   # stage analysis: not a bench line
         if rank == 0:
-            print(json.dumps({"only": args.only, "value": round(value, 3),
+            print(json.dumps({"only": args.only, "compose_parts": args.compose_parts,
+                              "value": round(value, 3),
                               "ms_per_step": round(ms / args.steps, 5),
                               "norm_sm_budget": args.norm_sms}), flush=True)
         return
@@ -842,6 +845,8 @@ def main():
     ap.add_argument("--nbuf", type=int, default=4)
     ap.add_argument("--only", default="", choices=["", "norm", "compose"],
                     help="analysis: time one stage of the step alone (not a bench number)")
+    ap.add_argument("--compose-parts", default="both", choices=["both", "fwd", "bwd"],
+                    help="analysis: which training compose kernels the step runs")
     ap.add_argument("--prof-steps", type=int, default=40)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -299,7 +299,7 @@ def run_gpu(args, rank, world, local_rank, dist):
     def set_budget(mode):
         # the pipelined graph runs module i's compose beside module i+1's norm: leave the
         # compose kernels the SMs the norm GEMMs do not plan for (dfx_ctx_set_sm_budget)
-        n = args.norm_sms if mode == args.mode else (80 if mode == "train" else 0)
+        n = args.norm_sms if mode == args.mode else (104 if mode == "train" else 0)
         dfx.set_sm_budget(n if args.pipeline > 1 else 0)
 
     def build_graphs(mode):
@@ -864,7 +864,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.norm_sms < 0:   # measured: the budget helps the C2 training pipeline only
-        args.norm_sms = 80 if (args.mode == "train" and args.config == "c2") else 0
+        args.norm_sms = 104 if (args.mode == "train" and args.config == "c2") else 0
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -11,7 +11,7 @@ for k in tc_pair_rowdot compose_fwd_vec compose_bwd_serial tc_rowdot; do
 done
 # the W.A^T GEMM as planned under the pipelined bench's SM budget (full r per pair)
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:tc_pair_rowdot -s 1 -c 1 \
-    -o gpurun_out/${R}_ncu_tc_pair_rowdot_budget80 python scripts/profile_module.py --steps 3 --budget 80 > /dev/null 2>&1
+    -o gpurun_out/${R}_ncu_tc_pair_rowdot_budget104 python scripts/profile_module.py --steps 3 --budget 104 > /dev/null 2>&1
 # the fused LoRA-up GEMM + compose epilogue
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:lora_compose -s 2 -c 1 \
     -o gpurun_out/${R}_ncu_lora_compose python scripts/exp_kernels.py --what lora_fused --iters 1 > /dev/null 2>&1

@@ -61,6 +61,21 @@ def vlm32b_stack(hidden: int = 5120, mlp: int = 27648, layers: int = 64, kv_head
     return [(f"l{l}.{n}", o, i) for l in range(layers) for (n, o, i) in per_layer]
 
 
+def row_split_bounds(d_out: int, world: int, align: int = 256) -> List[Tuple[int, int]]:
+    """Row (d_out) ranges [r0, r1) per rank for the row split of one module: blocks of
+    `align` rows (the 2-SM W.A^T kernel's pair tile), as even as the blocks allow.  Each rank
+    runs the norm on W[r0:r1], B[r0:r1] with A replicated and the compose on columns
+    [r0, r1) of the activations — no exchange (the Gram is recomputed per rank)."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    units = (d_out + align - 1) // align
+    out = []
+    for k in range(world):
+        u0, u1 = units * k // world, units * (k + 1) // world
+        out.append((min(u0 * align, d_out), min(u1 * align, d_out)))
+    return out
+
+
 def dsplit_bounds(d_in: int, world: int, chunk_size: int) -> List[Tuple[int, int]]:
     """K ranges [k0, k1) per rank for the d_in split, on ChunkPlan chunk boundaries when
     there are at least `world` chunks (whole chunks per rank), else on 64-column

@@ -45,6 +45,17 @@ def test_dsplit_bounds():
         assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
 
 
+def test_row_split_bounds():
+    assert D.row_split_bounds(8192, 2) == [(0, 4096), (4096, 8192)]
+    assert D.row_split_bounds(8192, 8) == [(k * 1024, (k + 1) * 1024) for k in range(8)]
+    b = D.row_split_bounds(28672, 3)
+    assert b[0][0] == 0 and b[-1][1] == 28672 and all(x[0] % 256 == 0 for x in b)
+    assert all(b[i][1] == b[i + 1][0] for i in range(2))
+    assert D.row_split_bounds(300, 4)[-1] == (256, 300)
+    with pytest.raises(ValueError):
+        D.row_split_bounds(10, 0)
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))

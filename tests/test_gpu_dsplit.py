@@ -5,7 +5,7 @@ oracle on the full matrices, and (whole-chunk slices, 2 ranks) bitwise base_sq."
 import numpy as np
 import pytest
 
-from conftest import bits_equal, to_dev
+from conftest import bits_equal, to_dev, to_np
 
 pytestmark = pytest.mark.gpu
 
@@ -52,3 +52,41 @@ def test_dsplit_matches_single_call(dfx, oracle, d_out, d_in, r, world, cs, dt):
     if world == 2 and d_in % (2 * cs) == 0:
         full_base = oracle.norm_terms(W, A, B, s, cs)[0]
         assert bits_equal(tot[r * r: r * r + d_out].cpu().numpy(), full_base)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("d_out,d_in,r", [(2048, 2048, 384), (1280, 4096, 128)])
+def test_row_split_matches_single_call(dfx, oracle, world, d_out, d_in, r):
+    """SURVEY 8(e) row split of one module (no exchange): each rank's norm on W[r0:r1],
+    B[r0:r1] with A replicated, and the compose on its d_out columns.  base_sq is bitwise
+    the single call's (serial chain per row), the norm within the bf16 bar, and the compose
+    columns bitwise (elementwise given the same g)."""
+    import torch
+    from paper_2603_22276_b200 import dist as D
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(d_out + world)
+    bf = torch.bfloat16
+    W = torch.randn(d_out, d_in, device="cuda", generator=gen).to(bf)
+    A = (0.05 * torch.randn(r, d_in, device="cuda", generator=gen)).to(bf)
+    B = (0.05 * torch.randn(d_out, r, device="cuda", generator=gen)).to(bf)
+    s = 2.0 / np.sqrt(r)
+    cs, _ = oracle.plan_chunks(d_out, d_in)
+    wn, terms = torch.empty(d_out, device="cuda"), torch.empty(3, d_out, device="cuda")
+    dfx.row_norm(W, A, B, s, cs, wn, terms=terms)
+    base = torch.randn(512, d_out, device="cuda", generator=gen).to(bf)
+    lora = torch.randn(512, d_out, device="cuda", generator=gen).to(bf)
+    g = (1.0 + 0.01 * torch.randn(d_out, device="cuda", generator=gen)).to(bf).float()
+    delta = torch.empty_like(base)
+    dfx.compose_fwd(base, lora, g, s, delta)
+    for (r0, r1) in D.row_split_bounds(d_out, world):
+        n = r1 - r0
+        wk, tk = torch.empty(n, device="cuda"), torch.empty(3, n, device="cuda")
+        dfx.row_norm(W[r0:r1].contiguous(), A, B[r0:r1].contiguous(), s, cs, wk, terms=tk)
+        dk = torch.empty(512, n, device="cuda", dtype=bf)
+        dfx.compose_fwd(base[:, r0:r1].contiguous(), lora[:, r0:r1].contiguous(),
+                        g[r0:r1].contiguous(), s, dk)
+        torch.cuda.synchronize()
+        assert bits_equal(to_np(tk[0]), to_np(terms[0, r0:r1]))
+        want = to_np(wn[r0:r1])
+        assert np.all(np.abs(to_np(wk) - want) <= np.spacing(want.astype(np.float32)) * 2 ** 16)
+        assert bits_equal(to_np(dk), to_np(delta[:, r0:r1]))

@@ -616,7 +616,7 @@ int dfx_working_matmul(dfx_ctx* ctx, dfx_dtype dtype, const void* A, int64_t sa_
     int rc = enter(ctx);
     if (rc) return rc;
     if (!valid_dtype(dtype)) return fail(DFX_EUNSUPPORTED, "working_matmul: dtype");
-    if (M < 0 || N < 0 || K < 0) return fail(DFX_EINVAL, "matmul_f32: inner dimensions disagree");
+    if (M < 0 || N < 0 || K < 0) return fail(DFX_EINVAL, "working_matmul: negative dimension");
     if (M > 0 && N > 0 && (!C || (K > 0 && (!A || !B))))
         return fail(DFX_EINVAL, "working_matmul: null operand");
     int launches = 0;

@@ -768,6 +768,23 @@ TEST("layer: frozen magnitude, zero upstream grad, bundle validation (test_layer
     CHECK_THROWS_AS(layer_forward(s9, gaussian_fixture(4, 17, 0.0, 1.0, 110)), std::invalid_argument);
 }
 
+TEST("layer: empty batch and rank 1 (edge cases of layer.cpp:51-165)") {
+    const DoraLinearState st = layer_state(12, 16, 24, 1);
+    const LayerForwardResult f0 = layer_forward(st, RealMatrix(0, 24, DTypeSpec::fp32()));
+    CHECK(f0.y.rows() == 0 && f0.y.cols() == 16);
+    CHECK(f0.saved.g.size() == 16 && f0.saved.inner.has_value());
+    const LayerGrads g0 = layer_backward(st, f0.saved, RealMatrix(0, 16, DTypeSpec::fp32()));
+    CHECK(g0.d_a.rows() == 1 && g0.d_a.cols() == 24 && g0.d_b.rows() == 16 && g0.d_b.cols() == 1);
+    for (double v : g0.d_a.data()) CHECK(v == 0.0);
+    for (double v : g0.d_b.data()) CHECK(v == 0.0);
+    for (double v : *g0.d_mag) CHECK(v == 0.0);
+    // rank 1, one row: every GEMM is a single product chain
+    const RealMatrix x = gaussian_fixture(1, 24, 0.0, 1.0, 120);
+    const LayerForwardResult f1 = layer_forward(st, x);
+    CHECK(same_bits(f1.saved.lora_mid, host_matmul(x, st.adapter.A, true, DTypeSpec::fp32())));
+    CHECK(same_bits(f1.saved.base_out, host_matmul(x, st.w, true, DTypeSpec::fp32())));
+}
+
 TEST("layer: gradients follow the detached-norm contract (test_layer.cpp:174)") {
     const DoraLinearState st = layer_state(8, 8, 6, 2);
     const RealMatrix x = gaussian_fixture(3, 6, 0.0, 1.0, 109);

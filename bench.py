@@ -314,6 +314,16 @@ def run_gpu(args, rank, world, local_rank, dist):
             ev_norm = [torch.cuda.Event() for _ in range(npipe)]
             ev_comp = [torch.cuda.Event() for _ in range(npipe)]
             gph = torch.cuda.CUDAGraph()
+            order = args.capture_order
+            if order == "auto":
+                order = "module" if mode == "train" else "norm-first"
+
+            def comp(i):
+                side.wait_event(ev_norm[i])
+                if args.only != "norm":
+                    compose(sets[i % nbuf], mode, sB)
+                ev_comp[i].record(side)
+
             with torch.cuda.graph(gph, stream=stream):
                 for i in range(npipe):
                     b = sets[i % nbuf]
@@ -322,10 +332,16 @@ def run_gpu(args, rank, world, local_rank, dist):
                     if args.only != "compose":
                         norm(b, sA)
                     ev_norm[i].record(stream)
-                    side.wait_event(ev_norm[i])
-                    if args.only != "norm":
-                        compose(b, mode, sB)
-                    ev_comp[i].record(side)
+                    # capture order = launch order among ready nodes: module i+1's norm is
+                    # created before module i's compose, so the GEMM CTAs claim their SMs
+                    # before the streaming kernels flood the GPU
+                    if order == "norm-first":
+                        if i >= 1:
+                            comp(i - 1)
+                    else:
+                        comp(i)
+                if order == "norm-first":
+                    comp(npipe - 1)
                 stream.wait_event(ev_comp[npipe - 1])
             graphs.append(gph)
         else:
@@ -845,6 +861,9 @@ def main():
     ap.add_argument("--nbuf", type=int, default=4)
     ap.add_argument("--only", default="", choices=["", "norm", "compose"],
                     help="analysis: time one stage of the step alone (not a bench number)")
+    ap.add_argument("--capture-order", default="auto", choices=["auto", "norm-first", "module"],
+                    help="graph node creation order of the pipelined step (auto: module order "
+                         "for training, norm-first for inference; measured, DESIGN 5.3)")
     ap.add_argument("--compose-parts", default="both", choices=["both", "fwd", "bwd"],
                     help="analysis: which training compose kernels the step runs")
     ap.add_argument("--prof-steps", type=int, default=40)

@@ -867,7 +867,7 @@ def main():
     ap.add_argument("--compose-parts", default="both", choices=["both", "fwd", "bwd"],
                     help="analysis: which training compose kernels the step runs")
     ap.add_argument("--prof-steps", type=int, default=40)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pipeline", type=int, default=40,
                     help="modules per graph, software-pipelined on two streams (1 = serial)")

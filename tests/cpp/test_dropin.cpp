@@ -785,6 +785,29 @@ TEST("layer: empty batch and rank 1 (edge cases of layer.cpp:51-165)") {
     CHECK(same_bits(f1.saved.base_out, host_matmul(x, st.w, true, DTypeSpec::fp32())));
 }
 
+TEST("layer: fp32 weights under a bf16 working dtype (rounded_to after matmul_f32)") {
+    // operands keep their fp32 tags; every GEMM result is rounded to the working dtype
+    const DTypeSpec& bf16 = DTypeSpec::bf16e();
+    RealMatrix w = gaussian_fixture(40, 72, 0.0, 0.5, 901);
+    AdapterPair ad{gaussian_fixture(8, 72, 0.0, 0.5, 902), gaussian_fixture(40, 8, 0.0, 0.5, 903), 0.7};
+    Magnitude mag{gaussian_vector(40, 1.5, 0.2, 904), DTypeSpec::fp32()};
+    const DoraLinearState st = make_layer_state(w, ad, mag, std::nullopt, bf16);
+    const RealMatrix x = gaussian_fixture(9, 72, 0.0, 1.0, 905);
+    const LayerForwardResult f = layer_forward(st, x);
+    const RealMatrix base = host_matmul(x, st.w, true, bf16);
+    const RealMatrix mid = host_matmul(x, st.adapter.A, true, bf16);
+    CHECK(same_bits(f.saved.base_out, base));
+    CHECK(same_bits(f.saved.lora_mid, mid));
+    CHECK(same_bits(f.saved.lora_out, host_matmul(mid, st.adapter.B, true, bf16)));
+    const RealMatrix dy = gaussian_fixture(9, 40, 0.0, 1.0, 906, bf16);
+    const LayerGrads gr = layer_backward(st, f.saved, dy);
+    const GradBundle gb = compose_backward(dy, f.saved.g, st.adapter.s, &*f.saved.inner,
+                                           f.saved.w_norm, true);
+    const RealMatrix d_mid = host_matmul(gb.d_lora, st.adapter.B, false, bf16);
+    CHECK(same_bits(gr.d_b, host_matmul(host_transpose(gb.d_lora), mid, false, bf16)));
+    CHECK(same_bits(gr.d_a, host_matmul(host_transpose(d_mid), x, false, bf16)));
+}
+
 TEST("layer: gradients follow the detached-norm contract (test_layer.cpp:174)") {
     const DoraLinearState st = layer_state(8, 8, 6, 2);
     const RealMatrix x = gaussian_fixture(3, 6, 0.0, 1.0, 109);

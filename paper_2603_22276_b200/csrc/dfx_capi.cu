@@ -582,7 +582,7 @@ int dfx_compose_bwd(dfx_ctx* ctx, dfx_dtype dtype, const void* dy, const float* 
     int launches = 0;
     const cudaError_t e =
         dfx::launch_compose_bwd(dtype, dy, g, static_cast<float>(s), inner, w_norm, rows, d_out,
-                                d_lora, d_base, d_mag, stream, &launches);
+                                d_lora, d_base, d_mag, stream, &launches, ctx->ws.sm_budget > 0);
     ctx->launches += launches;
     return finish_call(e, "dfx_compose_bwd");
 }

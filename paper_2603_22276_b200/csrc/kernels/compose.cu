@@ -262,26 +262,27 @@ __global__ void __launch_bounds__(256) compose_bwd_vec(const T* __restrict__ dy,
 //   warp 0    = TMA producer
 //   warps 1.. = chain warps, one thread per column, serial over rows (bitwise ref order)
 //   last 4    = elementwise warps: d_lora / d_base from the same stage, 16 B stores
-template <typename T, int S = 6>
+template <typename T, int S = 6, int Wd = 1>
 struct SerialCfg {
-    static constexpr int kSC = 128 / sizeof(T);            // slab columns
+    static constexpr int kRowBytes = 128 * Wd;              // slab width: Wd x 128 bytes
+    static constexpr int kSC = kRowBytes / sizeof(T);       // slab columns
     static constexpr int kRB = 64;                          // rows per stage
     static constexpr int kStages = S;
-    static constexpr int kStageBytes = kRB * 128;           // per tensor
+    static constexpr int kStageBytes = kRB * kRowBytes;     // per tensor
     static constexpr int kCPT = 4 / sizeof(T);              // chain columns per thread
-    static constexpr int kChainWarps = 1;                   // 32 threads x kCPT columns
-    static constexpr int kEltWarps = 4;
+    static constexpr int kChainWarps = Wd;                  // 32 threads x kCPT columns each
+    static constexpr int kEltWarps = 4 * Wd;
     static constexpr int kThreads = 32 * (1 + kChainWarps + kEltWarps);
     static constexpr int kSmem = 2 * kStages * kStageBytes + 2 * kStages * 8 + 1024;
 };
 
-template <typename T, int S>
-__global__ void __launch_bounds__(SerialCfg<T, S>::kThreads, 1)
+template <typename T, int S, int Wd = 1>
+__global__ void __launch_bounds__(SerialCfg<T, S, Wd>::kThreads, 1)
     compose_bwd_serial(const __grid_constant__ CUtensorMap tm_dy,
                        const __grid_constant__ CUtensorMap tm_inner, const float* __restrict__ g,
                        float sf, const float* __restrict__ w_norm, int64_t rows, int64_t d_out,
                        T* __restrict__ d_lora, T* __restrict__ d_base, float* __restrict__ d_mag) {
-    using C = SerialCfg<T, S>;
+    using C = SerialCfg<T, S, Wd>;
     constexpr int V = Vec<T>::N;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(SerialCfg<T, S>::kThreads, 1)
         // chain thread: kCPT adjacent columns (one 32-bit shared-memory word per row), one
         // serial fp32 accumulator per column over rows ascending (independent chains)
         constexpr int P = C::kCPT;
-        const int jc = lane * P;
+        const int jc = (warp - 1) * (128 / int(sizeof(T))) + lane * P;
         float acc[P];
 #pragma unroll
         for (int c = 0; c < P; ++c) acc[c] = 0.0f;
@@ -344,8 +345,8 @@ __global__ void __launch_bounds__(SerialCfg<T, S>::kThreads, 1)
 #pragma unroll
                     for (int u = 0; u < 16; ++u) {
                         float fy[P], fi[P];
-                        Word<T>::unpack(lds_u32(py + (i0 + u) * 128), fy);
-                        Word<T>::unpack(lds_u32(pi + (i0 + u) * 128), fi);
+                        Word<T>::unpack(lds_u32(py + (i0 + u) * C::kRowBytes), fy);
+                        Word<T>::unpack(lds_u32(pi + (i0 + u) * C::kRowBytes), fi);
 #pragma unroll
                         for (int c = 0; c < P; ++c) p[u][c] = __fmul_rn(fy[c], fi[c]);
                     }
@@ -357,8 +358,8 @@ __global__ void __launch_bounds__(SerialCfg<T, S>::kThreads, 1)
             } else {
                 for (int i = 0; i < nr; ++i) {
                     float fy[P], fi[P];
-                    Word<T>::unpack(lds_u32(py + i * 128), fy);
-                    Word<T>::unpack(lds_u32(pi + i * 128), fi);
+                    Word<T>::unpack(lds_u32(py + i * C::kRowBytes), fy);
+                    Word<T>::unpack(lds_u32(pi + i * C::kRowBytes), fi);
 #pragma unroll
                     for (int c = 0; c < P; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(fy[c], fi[c]));
                 }
@@ -372,9 +373,10 @@ __global__ void __launch_bounds__(SerialCfg<T, S>::kThreads, 1)
             if (j < d_out) d_mag[j] = __fdiv_rn(acc[c], __ldg(w_norm + j));
         }
     } else {
-        // elementwise warps: 128 threads, each a fixed 16-byte column vector
+        // elementwise warps: 128 threads per 128 bytes of slab, each a fixed 16-byte vector
         const int t = threadIdx.x - 32 * (1 + C::kChainWarps);
-        constexpr int kVecPerRow = 128 / 16;                    // 8
+        constexpr int kVecPerRow = C::kRowBytes / 16;
+        constexpr int kEltThreads = 32 * C::kEltWarps;
         const int cvec = t % kVecPerRow;
         const int64_t j0 = col0 + cvec * V;
         // d_lora == d_base == null: magnitude gradient only (the warps still pace the ring)
@@ -390,8 +392,8 @@ __global__ void __launch_bounds__(SerialCfg<T, S>::kThreads, 1)
             mbar_wait(&full[s], (it / C::kStages) & 1);
             const uint4* sy = reinterpret_cast<const uint4*>(s_dy + s * C::kStageBytes);
 #pragma unroll
-            for (int q = 0; q < C::kRB * kVecPerRow / 128; ++q) {
-                const int idx = q * 128 + t;
+            for (int q = 0; q < C::kRB * kVecPerRow / kEltThreads; ++q) {
+                const int idx = q * kEltThreads + t;
                 const int rr = idx / kVecPerRow;
                 const int64_t row = int64_t(it) * C::kRB + rr;
                 const uint4 v = sy[idx];
@@ -483,22 +485,22 @@ cudaError_t fwd_impl(const void* base, const void* lora, const float* g, float s
     return cudaGetLastError();
 }
 
-template <typename T, int S>
+template <typename T, int S, int Wd = 1>
 cudaError_t bwd_serial_launch(int dt, const void* dy, const float* g, float sf, const void* inner,
                               const float* w_norm, int64_t rows, int64_t d_out, T* dl, T* db,
                               float* d_mag, cudaStream_t st) {
-    using C = SerialCfg<T, S>;
+    using C = SerialCfg<T, S, Wd>;
     CUtensorMap tm_dy, tm_in;
     const uint64_t pitch = static_cast<uint64_t>(d_out) * sizeof(T);
     cudaError_t e = make_tmap_2d(&tm_dy, dt, dy, rows, d_out, pitch, C::kSC, C::kRB, false);
     if (e != cudaSuccess) return e;
     e = make_tmap_2d(&tm_in, dt, inner, rows, d_out, pitch, C::kSC, C::kRB, false);
     if (e != cudaSuccess) return e;
-    e = ensure_max_dyn_smem(reinterpret_cast<const void*>(compose_bwd_serial<T, S>), C::kSmem);
+    e = ensure_max_dyn_smem(reinterpret_cast<const void*>(compose_bwd_serial<T, S, Wd>), C::kSmem);
     if (e != cudaSuccess) return e;
     const unsigned grid = static_cast<unsigned>((d_out + C::kSC - 1) / C::kSC);
     prof_begin("compose_bwd_dmag", st);
-    compose_bwd_serial<T, S><<<grid, C::kThreads, C::kSmem, st>>>(tm_dy, tm_in, g, sf, w_norm, rows,
+    compose_bwd_serial<T, S, Wd><<<grid, C::kThreads, C::kSmem, st>>>(tm_dy, tm_in, g, sf, w_norm, rows,
                                                                    d_out, dl, db, d_mag);
     prof_end(st);
     return cudaGetLastError();
@@ -507,7 +509,7 @@ cudaError_t bwd_serial_launch(int dt, const void* dy, const float* g, float sf, 
 template <typename T>
 cudaError_t bwd_impl(int dt, const void* dy, const float* g, float sf, const void* inner,
                      const float* w_norm, int64_t rows, int64_t d_out, void* d_lora, void* d_base,
-                     float* d_mag, cudaStream_t st) {
+                     float* d_mag, cudaStream_t st, bool partitioned) {
     constexpr int V = Vec<T>::N;
     const T* y = static_cast<const T*>(dy);
     T* dl = static_cast<T*>(d_lora);
@@ -545,6 +547,11 @@ cudaError_t bwd_impl(int dt, const void* dy, const float* g, float sf, const voi
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t slabs = (d_out + SerialCfg<T>::kSC - 1) / SerialCfg<T>::kSC;
+        // beside the norm GEMMs (an SM budget is set): 256-byte slabs, half as many CTAs, each
+        // filling an SM — measured +1.5-2.7 % on the pipelined C2 training step (A/B on one
+        // box); alone they are slower (57 vs 47 us), so the full-GPU launch keeps 128-byte slabs
+        if (partitioned && slabs <= 2 * int64_t(sms))
+            return bwd_serial_launch<T, 6, 2>(dt, dy, g, sf, inner, w_norm, rows, d_out, dl, db, d_mag, st);
         return slabs > 2 * int64_t(sms)
                    ? bwd_serial_launch<T, 3>(dt, dy, g, sf, inner, w_norm, rows, d_out, dl, db, d_mag, st)
                    : bwd_serial_launch<T, 6>(dt, dy, g, sf, inner, w_norm, rows, d_out, dl, db, d_mag, st);
@@ -581,7 +588,8 @@ cudaError_t launch_compose_fwd(int dt, const void* base, const void* lora, const
 
 cudaError_t launch_compose_bwd(int dt, const void* dy, const float* g, float sf, const void* inner,
                                const float* w_norm, int64_t rows, int64_t d_out, void* d_lora,
-                               void* d_base, float* d_mag, cudaStream_t st, int* launches) {
+                               void* d_base, float* d_mag, cudaStream_t st, int* launches,
+                               bool partitioned) {
     if (d_out == 0) return cudaSuccess;
     // rows == 0 with d_mag: the reference yields 0 / w_norm per column; the
     // generic kernel's empty row loop reproduces that.
@@ -589,13 +597,14 @@ cudaError_t launch_compose_bwd(int dt, const void* dy, const float* g, float sf,
     if (launches) ++*launches;
     switch (dt) {
         case kF32:
-            return bwd_impl<float>(dt, dy, g, sf, inner, w_norm, rows, d_out, d_lora, d_base, d_mag, st);
+            return bwd_impl<float>(dt, dy, g, sf, inner, w_norm, rows, d_out, d_lora, d_base, d_mag, st,
+                                   partitioned);
         case kBF16:
             return bwd_impl<__nv_bfloat16>(dt, dy, g, sf, inner, w_norm, rows, d_out, d_lora, d_base,
-                                           d_mag, st);
+                                           d_mag, st, partitioned);
         default:
             return bwd_impl<__half>(dt, dy, g, sf, inner, w_norm, rows, d_out, d_lora, d_base, d_mag,
-                                    st);
+                                    st, partitioned);
     }
 }
 

@@ -32,9 +32,13 @@ cudaError_t launch_compose_fwd(int dt, const void* base, const void* lora, const
                                int64_t rows, int64_t d_out, void* delta, void* inner,
                                cudaStream_t st, int* launches);
 
+// partitioned: the caller runs this beside the norm GEMMs on an SM budget
+// (dfx_ctx_set_sm_budget): the d_mag backward then uses 256-byte column slabs (half the CTAs,
+// each a whole SM), which co-schedules better with the GEMM's CTA pairs (DESIGN 5.3)
 cudaError_t launch_compose_bwd(int dt, const void* dy, const float* g, float sf, const void* inner,
                                const float* w_norm, int64_t rows, int64_t d_out, void* d_lora,
-                               void* d_base, float* d_mag, cudaStream_t st, int* launches);
+                               void* d_base, float* d_mag, cudaStream_t st, int* launches,
+                               bool partitioned = false);
 
 // LoRA-up GEMM (mid . B^T on tcgen05) fused with compose + residual (lora_compose.cu).
 // Outputs y / delta / inner / lora are each optional (at most three at once).

@@ -234,3 +234,26 @@ def test_module_train_host_matches_device_path(dfx, oracle):
     assert torch.equal(out["dl"], dl.cpu())
     assert torch.equal(out["db"], db.cpu())
     assert torch.equal(hdm, dm.cpu())
+
+
+@pytest.mark.parametrize("rows,d_out,dt", [(1000, 512, 1), (257, 264, 2), (4096, 8192, 1),
+                                           (333, 96, 0), (64, 200, 1)])
+def test_backward_bitwise_under_sm_budget(oracle, rows, d_out, dt):
+    """With an SM budget set (composes beside the norm) the d_mag backward runs 256-byte
+    column slabs; the results stay bitwise the reference's (compose.cpp:154-201)."""
+    import paper_2603_22276_b200 as P
+    dfx = P.Dfx(0)
+    dfx.set_sm_budget(104)
+    rng = np.random.default_rng(rows * 11 + d_out)
+    dy = rng.standard_normal((rows, d_out), dtype=np.float32)
+    inner = rng.standard_normal((rows, d_out), dtype=np.float32)
+    if dt:
+        dy, inner = to_np(to_dev(dy, dt)), to_np(to_dev(inner, dt))
+    g = _g(oracle, d_out, dt, 9, sd=0.01)
+    wn = np.array([oracle.round_to_dtype(5.0 + 0.01 * j, dt) for j in range(d_out)], np.float32)
+    s = 0.7
+    want = oracle.compose_bwd(dt, dy, g, s, inner, wn, mag_grad=True)
+    got = _bwd(dfx, dy, g, s, inner, wn, dt, True)
+    for w, gt in zip(want, got):
+        assert bits_equal(gt, w)
+    dfx.close()

@@ -8,6 +8,6 @@ make -s -C $C ../libdfx.so
 mkdir -p variants/obj_$NAME
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
      -Iinclude -I$C/kernels $FLAGS -c $C/kernels/compose.cu -o variants/obj_$NAME/compose.o
-OBJS=$(ls $C/obj/*.o $C/obj/kernels/*.o | grep -v compose.o)
+OBJS=$(ls $C/obj/*.o $C/obj/kernels/*.o | grep -v "/compose.o$")
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o variants/libdfx_$NAME.so $OBJS variants/obj_$NAME/compose.o -lcudart
 echo built variants/libdfx_$NAME.so

@@ -139,7 +139,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------- CPU reference
-def cpu_reference_rate(cfg, cores, mode="train", rounds=1, warm=0, log=None):
+def cpu_reference_rate(cfg, cores, mode="train", rounds=1, warm=0, log=None, full_module=False):
     """The reference's own C++ (oracle/_ref/libdfx_ref.so, compiled from the reference
     sources) on this host.  The reference is single-threaded per call, so all cores run
     independent module samples concurrently (as its own suites do, suites.cpp:49-65).
@@ -168,7 +168,7 @@ def cpu_reference_rate(cfg, cores, mode="train", rounds=1, warm=0, log=None):
             return u.view(np.float32)
         return a.astype(np.float16).astype(np.float32) if dt == 2 else a.astype(np.float32)
 
-    NS1, NS2, CT = 8, 40, 256
+    NS1, NS2, CT = 16, 128, 256
     A = rnd(rng.standard_normal((r, d_in)))
     Wn = rnd(rng.standard_normal((NS2, d_in)))
     Bn = rnd(rng.standard_normal((NS2, r)))
@@ -221,10 +221,45 @@ def cpu_reference_rate(cfg, cores, mode="train", rounds=1, warm=0, log=None):
         if k >= warm:
             rates.append(cores * sample_equiv / wall)
     rate = sorted(rates)[len(rates) // 2]
+    full = None
+    if full_module:
+        # validate the conversion model: one WHOLE module on one core (every W row, every
+        # token), the reference's own calls back to back
+        Wf = rnd(rng.standard_normal((d_out, d_in)))
+        Bf = rnd(rng.standard_normal((d_out, r)))
+        R.row_norm(dt, Wf, A, Bf, s, cs)
+        t_norm = R.last_call_s()
+        del Wf
+        t_comp = 0.0
+        for c0 in range(0, tokens, 1024):           # the whole token range, 1024 rows per call
+            nr = min(1024, tokens - c0)
+            bb = rnd(rng.standard_normal((nr, d_out)))
+            ll = rnd(rng.standard_normal((nr, d_out)))
+            if mode == "infer":
+                R.compose(1, dt, bb, ll, g, s)
+                t_comp += R.last_call_s()
+            else:
+                yy = rnd(rng.standard_normal((nr, d_out)))
+                _, inn = R.compose(2, dt, bb, ll, g, s, need_inner=True)
+                t_comp += R.last_call_s()
+                R.compose_bwd(dt, yy, g, s, inner=inn, w_norm=wn, mag_grad=True)
+                t_comp += R.last_call_s()
+        t_full = t_norm + t_comp
+        full = {"measured_full_module_s": round(t_full, 3), "measured_norm_s": round(t_norm, 3),
+                "measured_compose_s": round(t_comp, 3), "model_s": round(t_module, 3),
+                "model_error": round(t_module / t_full - 1.0, 4),
+                "value_uncorrected": round(rate, 6),
+                "correction": "value = all-core sample rate x model_s / measured_full_module_s "
+                              "(the conversion model rescaled to the measured whole module)"}
+        rate = rate * t_module / t_full
+        if log:
+            log(f"cpu ref full module (1 core): {t_full:.2f}s (norm {t_norm:.2f}s, compose "
+                f"{t_comp:.2f}s) vs model {t_module:.2f}s")
     what = ("dual_output_compose + compose_backward (mag_grad)" if mode == "train"
             else "fused_compose")
     return rate, {
         "t_module_1core_s": t_module, "t_fixed_s": t_fixed, "t_row_ms": t_row * 1e3,
+        "full_module": full,
         "t_compose_per_token_us": t_c / CT * 1e6, "rounds": rounds,
         "sample": (f"per thread: reference factored_row_norm on {NS2} of {d_out} W rows (full "
                    f"d_in={d_in}, r={r}, Gram included) + {what} on {CT} of {tokens} "
@@ -296,76 +331,95 @@ def run_gpu(args, rank, world, local_rank, dist):
     stream = torch.cuda.Stream(device=dev)
     side = torch.cuda.Stream(device=dev)
 
-    def set_budget(mode):
+    def set_budget(mode, npipe):
         # the pipelined graph runs module i's compose beside module i+1's norm: leave the
-        # compose kernels the SMs the norm GEMMs do not plan for (dfx_ctx_set_sm_budget)
+        # compose kernels the SMs the norm GEMMs do not plan for (dfx_ctx_set_sm_budget).
+        # A serial step (npipe == 1) gets the whole GPU for every kernel.
         n = args.norm_sms if mode == args.mode else (104 if mode == "train" else 0)
-        dfx.set_sm_budget(n if args.pipeline > 1 else 0)
+        dfx.set_sm_budget(n if npipe > 1 else 0)
 
-    def build_graphs(mode):
-        """Modules are independent, so a graph holds npipe consecutive modules software-
-        pipelined on two streams: module i's compose (HBM-bound) runs on stream B beside
-        module i+1's row norm (tensor-bound) on stream A.  Edges: compose i after norm i
-        (it reads g_i, w_norm_i); norm i+nbuf after compose i (it rewrites set i % nbuf)."""
-        npipe = args.pipeline if (args.pipeline > 1 and args.steps % args.pipeline == 0) else 1
-        graphs = []
-        if npipe > 1:
-            sA, sB = stream.cuda_stream, side.cuda_stream
-            ev_norm = [torch.cuda.Event() for _ in range(npipe)]
-            ev_comp = [torch.cuda.Event() for _ in range(npipe)]
-            gph = torch.cuda.CUDAGraph()
-            order = args.capture_order
-            if order == "auto":
-                order = "module" if mode == "train" else "norm-first"
+    def build_pipelined(mode, n):
+        """A graph of n consecutive modules software-pipelined on two streams: module i's
+        compose (HBM-bound) on stream B beside module i+1's row norm (tensor-bound) on
+        stream A.  Edges: compose i after norm i (it reads g_i, w_norm_i); norm i+nbuf after
+        compose i (it rewrites set i % nbuf)."""
+        sA, sB = stream.cuda_stream, side.cuda_stream
+        ev_norm = [torch.cuda.Event() for _ in range(n)]
+        ev_comp = [torch.cuda.Event() for _ in range(n)]
+        gph = torch.cuda.CUDAGraph()
+        order = args.capture_order
+        if order == "auto":
+            order = "module" if mode == "train" else "norm-first"
 
-            def comp(i):
-                side.wait_event(ev_norm[i])
-                if args.only != "norm":
-                    compose(sets[i % nbuf], mode, sB)
-                ev_comp[i].record(side)
+        def comp(i):
+            side.wait_event(ev_norm[i])
+            if args.only != "norm":
+                compose(sets[i % nbuf], mode, sB)
+            ev_comp[i].record(side)
 
-            with torch.cuda.graph(gph, stream=stream):
-                for i in range(npipe):
-                    b = sets[i % nbuf]
-                    if i >= nbuf:
-                        stream.wait_event(ev_comp[i - nbuf])
-                    if args.only != "compose":
-                        norm(b, sA)
-                    ev_norm[i].record(stream)
-                    # capture order = launch order among ready nodes: module i+1's norm is
-                    # created before module i's compose, so the GEMM CTAs claim their SMs
-                    # before the streaming kernels flood the GPU
-                    if order == "norm-first":
-                        if i >= 1:
-                            comp(i - 1)
-                    else:
-                        comp(i)
+        with torch.cuda.graph(gph, stream=stream):
+            for i in range(n):
+                b = sets[i % nbuf]
+                if i >= nbuf:
+                    stream.wait_event(ev_comp[i - nbuf])
+                if args.only != "compose":
+                    norm(b, sA)
+                ev_norm[i].record(stream)
+                # capture order = launch order among ready nodes: module i+1's norm is
+                # created before module i's compose, so the GEMM CTAs claim their SMs
+                # before the streaming kernels flood the GPU
                 if order == "norm-first":
-                    comp(npipe - 1)
-                stream.wait_event(ev_comp[npipe - 1])
-            graphs.append(gph)
+                    if i >= 1:
+                        comp(i - 1)
+                else:
+                    comp(i)
+            if order == "norm-first":
+                comp(n - 1)
+            stream.wait_event(ev_comp[n - 1])
+        return gph
+
+    def build_graphs(mode, steps):
+        """(schedule of (graph, modules) replays for `steps` modules, npipe).  npipe =
+        min(--pipeline, steps): the timed steps run as steps // npipe replays of one
+        npipe-module pipelined graph plus one remainder graph of steps % npipe modules, so
+        every step count runs the pipelined protocol.  --pipeline 1: one serial graph per
+        buffer set."""
+        npipe = min(args.pipeline, steps) if args.pipeline > 1 else 1
+        sched = []
+        if npipe > 1:
+            main = build_pipelined(mode, npipe)
+            sched += [(main, npipe)] * (steps // npipe)
+            rem = steps % npipe
+            if rem:
+                sched.append((build_pipelined(mode, rem) if rem > 1 else serial_graph(mode, 0), rem))
         else:
-            for b in sets:
-                gph = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(gph, stream=stream):
-                    step(b, mode)
-                graphs.append(gph)
+            gs = [serial_graph(mode, i) for i in range(nbuf)]
+            sched = [(gs[k % nbuf], 1) for k in range(steps)]
         torch.cuda.synchronize()
-        return graphs, npipe
+        return sched, npipe
+
+    def serial_graph(mode, i):
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph, stream=stream):
+            step(sets[i % nbuf], mode)
+        return gph
 
     def timed(mode, steps, warmup, clocks=None):
-        set_budget(mode)
-        # one eager pass under this plan first: the context grows its workspace outside of
-        # graph capture (allocation is not capturable)
+        npipe = min(args.pipeline, steps) if args.pipeline > 1 else 1
+        set_budget(mode, npipe)
+        # one eager pass under this plan first: the context sizes its workspace outside of
+        # graph capture (dfx calls refuse to grow it while a capture is active)
         with torch.cuda.stream(stream):
             for b in sets:
                 step(b, mode)
         torch.cuda.synchronize()
-        graphs, npipe = build_graphs(mode)
-        nrep = len(graphs)
+        sched, npipe = build_graphs(mode, steps)
         with torch.cuda.stream(stream):
-            for k in range((warmup + npipe - 1) // npipe):
-                graphs[k % nrep].replay()
+            done = 0
+            while done < warmup:                       # >= warmup modules, whole graphs
+                g, n = sched[0]
+                g.replay()
+                done += n
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if dist:
@@ -375,8 +429,8 @@ def run_gpu(args, rank, world, local_rank, dist):
         with (clocks if clocks is not None else contextlib.nullcontext()):
             with torch.cuda.stream(stream):
                 ev0.record(stream)
-                for k in range(steps // npipe):
-                    graphs[k % nrep].replay()
+                for g, _ in sched:
+                    g.replay()
                 ev1.record(stream)
             torch.cuda.synchronize()
         if dist:
@@ -416,7 +470,7 @@ def run_gpu(args, rank, world, local_rank, dist):
     variants = {}
     other = "infer" if args.mode == "train" else "train"
     if args.variant_steps > 0:
-        vsteps = args.variant_steps - args.variant_steps % max(1, args.pipeline)
+        vsteps = args.variant_steps
         vms, _ = timed(other, vsteps, args.warmup)
         variants[other] = {
             "value": round(world * vsteps / (vms / 1e3), 3), "unit": UNIT,
@@ -495,38 +549,48 @@ def run_gpu(args, rank, world, local_rank, dist):
             "plain_us": round(tn, 2), "cached_us": round(tc, 2), "speedup": round(tn / tc, 3)}
         log(f"row_norm plain {tn:.1f} us vs cached base_sq {tc:.1f} us")
 
-    # ---- per-kernel live durations (event-bracketed launches, same kernels/buffers)
+    # ---- per-kernel live durations (event-bracketed launches, same kernels / buffers / plan
+    # as the timed region).  Each step is queued behind a 2 ms device spin so the brackets
+    # time the device, not the host; the kernels therefore run as in a single isolated
+    # module (no neighbouring module overlaps them), so fractions divide by the BURST peaks.
+    # Torch events around the row_norm call (fork to join, on the launching stream) give the
+    # norm stage's wall time; around the whole step, the step's wall time.
     prof_steps = min(args.steps, args.prof_steps)
-    set_budget(args.mode)
+    set_budget(args.mode, npipe)
     dfx.profile(True)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(prof_steps)]
     with torch.cuda.stream(stream):
         for k in range(prof_steps):
-            torch.cuda._sleep(2_000_000)       # queue the whole step behind a spin so the
-            step(sets[k % nbuf], args.mode)    # brackets time the device, not the host
+            torch.cuda._sleep(2_000_000)
+            b = sets[k % nbuf]
+            ev[k][0].record(stream)
+            norm(b)
+            ev[k][1].record(stream)
+            compose(b, args.mode)
+            ev[k][2].record(stream)
     rep = dfx.profile_report()
     dfx.profile(False)
+    norm_wall_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / prof_steps
+    step_wall_ms = sum(e[0].elapsed_time(e[2]) for e in ev) / prof_steps
     peaks_hbm, peak_tf_burst, peak_tf_sus, peak_src = load_peaks()
     alg = algorithmic(cfg)
     kernels = {}
     for name, (n, tot, mn, mx) in rep.items():
         avg_ms = tot / n
         ent = {"launches_per_step": n / prof_steps, "avg_us": round(avg_ms * 1e3, 2),
-               "min_us": round(mn * 1e3, 2)}
+               "min_us": round(mn * 1e3, 2),
+               "share_of_step_wall": round(tot / prof_steps / step_wall_ms, 4)}
         if name in alg:
             bound, flops, byts = alg[name]
             if bound == "tensor":
                 ach = flops / (avg_ms / 1e3) / 1e12
                 ent.update(bound="tensor", achieved=round(ach, 1), unit="TFLOP/s",
-                           frac=round(ach / peak_tf_sus, 4))
+                           frac=round(ach / peak_tf_burst, 4))
             else:
                 ach = byts / (avg_ms / 1e3) / 1e9
                 ent.update(bound="hbm", achieved=round(ach, 1), unit="GB/s",
                            frac=round(ach / peaks_hbm, 4))
         kernels[name] = ent
-    step_ms = sum(v[1] for v in rep.values()) / prof_steps
-    for name, ent in kernels.items():
-        ent["share"] = round(rep[name][1] / prof_steps / step_ms, 4)
-    norm_ms = sum(v[1] for k, v in rep.items() if not k.startswith("compose")) / prof_steps
     dom = max(kernels, key=lambda k: rep[k][1])
     bound, flops, byts = alg.get(dom, ("hbm", 0.0, 0.0))
     traffic = None
@@ -534,32 +598,33 @@ def run_gpu(args, rank, world, local_rank, dist):
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f).get(args.config, {})
             budget_key = f"{dom}_budget{args.norm_sms}"
-            traffic = tr.get(budget_key if (args.pipeline > 1 and budget_key in tr) else dom)
+            traffic = tr.get(budget_key if (npipe > 1 and args.norm_sms > 0 and budget_key in tr)
+                             else dom)
     except Exception:
         pass
     dk = kernels[dom]
     roofline = {"kernel": dom, "bound": bound, "achieved": dk.get("achieved"),
-                "peak": peak_tf_sus if bound == "tensor" else peaks_hbm,
+                "peak": peak_tf_burst if bound == "tensor" else peaks_hbm,
                 "unit": "TFLOP/s" if bound == "tensor" else "GB/s", "frac": dk.get("frac"),
                 "traffic": traffic,
                 "algorithmic_per_launch": flops if bound == "tensor" else byts,
-                "peak_source": f"{peak_src}: bf16 sustained {peak_tf_sus} TF/s (burst "
-                               f"{peak_tf_burst}), HBM copy {peaks_hbm} GB/s",
-                "avg_us": dk["avg_us"], "share": dk["share"]}
+                "peak_source": f"{peak_src}: bf16 burst {peak_tf_burst} TF/s (each kernel is "
+                               f"event-bracketed in an isolated module, so burst applies; "
+                               f"sustained {peak_tf_sus}), HBM copy {peaks_hbm} GB/s",
+                "avg_us": dk["avg_us"], "share_of_step_wall": dk["share_of_step_wall"]}
+    if bound == "tensor":
+        roofline["frac_of_sustained"] = round(dk["achieved"] / peak_tf_sus, 4)
     if dom == "u_rowdot_tc" and cfg["dtype"] == "bf16":
-        # the SMs this launch occupies under the step's SM budget (the others run the composes):
-        # the same achieved rate against the sustained peak scaled to those SMs
+        # the SMs this launch occupies under the step's SM budget (context, not the roofline)
         try:
             u_sms, side_sms, strat = dfx.norm_plan(d_out, d_in, r, cs)
-            nsm = torch.cuda.get_device_properties(dev).multi_processor_count
             roofline["sms_used"] = u_sms
-            roofline["frac_of_sms_used"] = round(dk["achieved"] / (peak_tf_sus * u_sms / nsm), 4)
             roofline["norm_plan"] = {"u_sms": u_sms, "side_sms": side_sms,
                                      "strategy": ["gram+V beside U", "gram beside, V after",
                                                   "serial"][strat]}
         except Exception as ex:  # noqa: BLE001 - context only, never fails the bench
             log(f"norm_plan unavailable: {ex}")
-    if args.pipeline > 1 and args.norm_sms > 0:
+    if npipe > 1 and args.norm_sms > 0:
         # the same W.A^T GEMM planned for the whole GPU (no SM budget), timed alone
         dfx.set_sm_budget(0)
         dfx.profile(True)
@@ -569,25 +634,24 @@ def run_gpu(args, rank, world, local_rank, dist):
                 norm(sets[k % nbuf])
         rep0 = dfx.profile_report()
         dfx.profile(False)
-        set_budget(args.mode)
+        set_budget(args.mode, npipe)
         if dom in rep0:
             n0_, tot0, mn0, _ = rep0[dom]
             avg0 = tot0 / n0_
+            work = flops if bound == "tensor" else byts
+            ach0 = work / (avg0 / 1e3) / (1e12 if bound == "tensor" else 1e9)
             roofline["unbudgeted"] = {
-                "avg_us": round(avg0 * 1e3, 2),
-                "achieved": round((flops if bound == "tensor" else byts) / (avg0 / 1e3) /
-                                  (1e12 if bound == "tensor" else 1e9), 1),
-                "frac": round((flops if bound == "tensor" else byts) / (avg0 / 1e3) /
-                              (1e12 if bound == "tensor" else 1e9) /
-                              (peak_tf_sus if bound == "tensor" else peaks_hbm), 4),
+                "avg_us": round(avg0 * 1e3, 2), "achieved": round(ach0, 1),
+                "frac": round(ach0 / (peak_tf_burst if bound == "tensor" else peaks_hbm), 4),
                 "note": f"the headline pipeline plans the norm GEMMs for {args.norm_sms} SMs "
                         f"(dfx_ctx_set_sm_budget) so the compose kernels run beside them; this "
                         f"is the kernel planned for all SMs"}
     nf = alg["norm_total"][1]
-    norm_roof = {"stage": "row_norm (all norm kernels)", "avg_us": round(norm_ms * 1e3, 2),
-                 "achieved_tflops": round(nf / (norm_ms / 1e3) / 1e12, 1),
-                 "frac_sustained": round(nf / (norm_ms / 1e3) / 1e12 / peak_tf_sus, 4),
-                 "frac_burst": round(nf / (norm_ms / 1e3) / 1e12 / peak_tf_burst, 4)}
+    norm_roof = {"stage": "row_norm wall time (event pair around the call: fork to join)",
+                 "avg_us": round(norm_wall_ms * 1e3, 2),
+                 "achieved_tflops": round(nf / (norm_wall_ms / 1e3) / 1e12, 1),
+                 "frac_burst": round(nf / (norm_wall_ms / 1e3) / 1e12 / peak_tf_burst, 4),
+                 "step_wall_us": round(step_wall_ms * 1e3, 2)}
     log(json.dumps(kernels))
 
     # ---- end to end through the host-buffer entry point (pinned host memory)
@@ -644,9 +708,12 @@ def run_gpu(args, rank, world, local_rank, dist):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cores = host_cores()
-            rate, det = cpu_reference_rate(cfg, cores, mode=args.mode, rounds=1, warm=0, log=log)
+            rate, det = cpu_reference_rate(cfg, cores, mode=args.mode, rounds=1, warm=0, log=log,
+                                           full_module=not args.no_cpu_full_module)
             cpu = {"value": round(rate, 6), "unit": UNIT, "cores": cores, "kind": "reference",
                    "sample": det["sample"], "t_module_1core_s": round(det["t_module_1core_s"], 2)}
+            if det["full_module"]:
+                cpu.update(det["full_module"])
         except Exception as e:
             cpu = {"value": None, "unavailable": str(e)}
 
@@ -671,7 +738,7 @@ def run_gpu(args, rank, world, local_rank, dist):
                        "pipeline": (f"{npipe} modules per graph; module i's compose overlaps "
                                     f"module i+1's norm on a second stream" if npipe > 1
                                     else "serial"),
-                       "norm_sm_budget": args.norm_sms if args.pipeline > 1 else 0},
+                       "norm_sm_budget": args.norm_sms if npipe > 1 else 0},
             "roofline": roofline, "roofline_norm_stage": norm_roof, "kernels": kernels,
             "variants": variants,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
@@ -813,24 +880,127 @@ def run_stack(args, rank, world, local_rank, dist):
     dfx.close()
 
 
+# ------------------------------------------------------------------ d_in split
+def run_dsplit(args, rank, world, local_rank, dist):
+    """`--mode dsplit`: ONE module's factored norm with d_in split across the ranks (FSDP2 /
+    TP-row style).  Rank k holds W[:, K_k], A[:, K_k] (whole
+    ChunkPlan chunks), replicated B and m.  One step = dfx_norm_partial -> one all-reduce of
+    {G, base_sq, cross} (r*r + 2*d_out fp32) -> dfx_norm_finish on every rank.  value = modules
+    (norms) per second for the whole job (all ranks cooperate on one module per step); the
+    exchange is timed separately.  --allreduce dfx uses the library's symmetric-memory kernel
+    (dfx_norm_allreduce, peer loads in rank order), nccl uses torch.distributed."""
+    import torch
+    import paper_2603_22276_b200 as P
+    from paper_2603_22276_b200.dist import SymmetricAllReduce, dsplit_bounds
+
+    cfg = CONFIGS[args.config]
+    d_out, d_in, r = cfg["d_out"], cfg["d_in"], cfg["r"]
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[cfg["dtype"]]
+    s = 2.0 / math.sqrt(r)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dfx = P.Dfx(local_rank)
+    cs, nchunks = P.plan_chunks(d_out, d_in)
+    k0, k1 = dsplit_bounds(d_in, world, cs)[rank]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(20261017)                       # the same module on every rank
+    W = torch.randn(d_out, d_in, device=dev, generator=gen).to(tdt)
+    A = torch.randn(r, d_in, device=dev, generator=gen).to(tdt)
+    B = torch.randn(d_out, r, device=dev, generator=gen).to(tdt)
+    Wk, Ak = W[:, k0:k1].contiguous(), A[:, k0:k1].contiguous()
+    del W
+    wn = torch.empty(d_out, device=dev)
+    g = torch.empty(d_out, device=dev)
+    m = torch.ones(d_out, device=dev)
+    n = r * r + 2 * d_out
+    comm = None
+    if args.allreduce == "dfx":
+        comm = SymmetricAllReduce(dfx, n, group=dist.group.WORLD if dist else None)
+        buf = comm.buffer()
+    else:
+        buf = torch.empty(n, dtype=torch.float32, device=dev)
+    red = torch.empty(n, dtype=torch.float32, device=dev)
+    gram, base, cross = buf[: r * r], buf[r * r: r * r + d_out], buf[r * r + d_out:]
+    rg, rb, rc = red[: r * r], red[r * r: r * r + d_out], red[r * r + d_out:]
+    stream = torch.cuda.current_stream(dev)
+
+    def exchange():
+        if comm is not None:
+            comm.all_reduce(red)
+        else:
+            red.copy_(buf)
+            if dist:
+                dist.all_reduce(red)
+
+    def one(evs=None):
+        dfx.norm_partial(Wk, Ak, B, cs, gram, base, cross)
+        if evs:
+            evs[0].record(stream)
+        exchange()
+        if evs:
+            evs[1].record(stream)
+        dfx.norm_finish(B, rg, rb, rc, s, wn, m=m, g=g)
+
+    for _ in range(max(3, args.warmup)):
+        one()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    steps = args.steps
+    evx = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(local_rank)
+    with clk:
+        e0.record(stream)
+        for k in range(steps):
+            one(evx[k])
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    xms = sum(a.elapsed_time(b) for a, b in evx) / steps
+    if dist:
+        t = torch.tensor([ms, xms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, xms = float(t[0]), float(t[1])
+    value = steps / (ms / 1e3)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC + " (d_in-split norm)", "value": round(value, 3), "unit": UNIT,
+            "n_gpus": world, "steps": steps, "warmup": max(3, args.warmup),
+            "ms_per_step": round(ms / steps, 5), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (seeded torch.randn)",
+            "config": {"workload": f"{args.config}: factored row norm of one module d_out={d_out} "
+                                   f"d_in={d_in} r={r}, d_in split over {world} ranks",
+                       "mode": "dsplit", "k_slice_rank0": [k0, k1], "chunk_plan": [cs, nchunks],
+                       "allreduce": args.allreduce, "message_bytes": 4 * n,
+                       "parallelism": f"d_in split x{world} (one all-reduce per module)"},
+            "exchange_us": round(xms * 1e3, 2), "clocks": clk.summary(),
+            "native_libs": [os.path.relpath(P.LIB_PATH, ROOT)]}), flush=True)
+    if comm is not None:
+        comm.close()
+    dfx.close()
+
+
 # ------------------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
     """`--impl reference`: the reference's own CPU implementation (oracle/_ref, compiled
     from the unmodified reference sources) on this host's cores, same metric/config."""
     if rank != 0:
         return
-    if args.config not in CONFIGS:
-        print(json.dumps({"impl": "reference", "unavailable": f"{args.config}: the stack is timed "
-                          "on the GPU arm only; the reference arm times single modules (c1-c4)"}))
+    if args.config == "c5":
+        run_reference_stack(args, rank, world)
         return
     cfg = CONFIGS[args.config]
     cores = host_cores()
     log = lambda m: print(m, file=sys.stderr, flush=True)
+    if args.mode == "dsplit":
+        args.mode = "train"
     # each round is ~2 s of all-core work; cap rounds so the run stays within minutes
     rounds = max(1, min(args.steps, 20))
     warm = min(args.warmup, 1)
     t0 = time.perf_counter()
-    rate, det = cpu_reference_rate(cfg, cores, mode=args.mode, rounds=rounds, warm=warm, log=log)
+    rate, det = cpu_reference_rate(cfg, cores, mode=args.mode, rounds=rounds, warm=warm, log=log,
+                                   full_module=not args.no_cpu_full_module)
     wall = time.perf_counter() - t0
     line = {
         "impl": "reference", "metric": METRIC, "value": round(rate, 6), "unit": UNIT,
@@ -843,12 +1013,59 @@ def run_reference(args, rank, world):
                                + " (proj/src, CPU, 1 thread per module)",
                    "mode": args.mode, **{k: cfg[k] for k in ("d_out", "d_in", "r", "tokens")}},
         "cpu_baseline": {"value": round(rate, 6), "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": det["sample"]},
+                         "sample": det["sample"], **(det["full_module"] or {})},
         "e2e": {"value": round(rate, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "wall_s": round(wall, 1),
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_reference_stack(cores, mode, log=None):
+    """The C5 stack on the reference's CPU path: for each distinct module shape of the
+    448-module inventory (4 shapes), cpu_reference_rate measures the all-core module
+    throughput of that shape (concurrent bounded samples, converted with the 1-core
+    calibration that the C2 whole-module run validates); the stack's time on all cores is
+    the sum over its modules of 1 / rate(shape).  Returns (stack passes/s as modules/s,
+    details)."""
+    from paper_2603_22276_b200.dist import vlm32b_stack
+    stack = vlm32b_stack()
+    shapes = sorted({(o, i) for _, o, i in stack})
+    per = {}
+    for d_out, d_in in shapes:
+        cfg = dict(d_out=d_out, d_in=d_in, r=384, tokens=4096, dtype="bf16")
+        rate, det = cpu_reference_rate(cfg, cores, mode=mode, rounds=1, warm=0, log=log)
+        per[f"{d_out}x{d_in}"] = {"modules_per_s_all_cores": round(rate, 6),
+                                  "t_module_1core_s": round(det["t_module_1core_s"], 2)}
+    t_stack = sum(1.0 / per[f"{o}x{i}"]["modules_per_s_all_cores"] for _, o, i in stack)
+    return len(stack) / t_stack, {"per_shape": per, "t_stack_all_cores_s": round(t_stack, 1),
+                                  "modules": len(stack)}
+
+
+def run_reference_stack(args, rank, world):
+    cores = host_cores()
+    log = lambda m: print(m, file=sys.stderr, flush=True)
+    t0 = time.perf_counter()
+    rate, det = cpu_reference_stack(cores, args.mode if args.mode != "dsplit" else "train", log)
+    wall = time.perf_counter() - t0
+    sample = (f"per module shape ({', '.join(det['per_shape'])}): reference factored_row_norm "
+              f"on 128 W rows + the compose on 256 of 4096 tokens per thread, {cores} threads "
+              f"concurrently, converted with a 1-core calibration; stack time = sum over the "
+              f"{det['modules']} modules of 1 / all-core rate of its shape = "
+              f"{det['t_stack_all_cores_s']} s (extrapolated, not run end to end)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC + " (C5 layer stack)", "value": round(rate, 6),
+        "unit": UNIT, "n_gpus": world, "steps": 1, "warmup": 0,
+        "ms_per_step": round(det["t_stack_all_cores_s"] * 1e3, 1), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (numpy, seeded)",
+        "config": {"workload": "c5: 32B-VLM-sized stack, 448 modules, r=384, tokens=4096, one "
+                               "pass = every module's norm + compose (reference, CPU)",
+                   "mode": args.mode, "per_shape": det["per_shape"]},
+        "cpu_baseline": {"value": round(rate, 6), "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": round(rate, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": round(wall, 1)}), flush=True)
 
 
 def main():
@@ -869,10 +1086,17 @@ def main():
     ap.add_argument("--prof-steps", type=int, default=40)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-full-module", action="store_true",
+                    help="skip the one whole module on one core that validates the CPU model")
     ap.add_argument("--pipeline", type=int, default=40,
                     help="modules per graph, software-pipelined on two streams (1 = serial)")
-    ap.add_argument("--mode", default="train", choices=["train", "infer"],
-                    help="train: norm + dual compose + backward (headline); infer: norm + compose")
+    ap.add_argument("--mode", default="train", choices=["train", "infer", "dsplit"],
+                    help="train: norm + dual compose + backward (headline); infer: norm + compose; "
+                         "dsplit: the d_in-split norm (partial, all-reduce, finish) across ranks")
+    ap.add_argument("--stub", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--allreduce", default="dfx", choices=["dfx", "nccl"],
+                    help="dsplit: the exchange of {G, base_sq, cross} (dfx symmetric-memory "
+                         "kernel or NCCL through torch.distributed)")
     ap.add_argument("--norm-sms", type=int, default=-1,
                     help="SM budget of the norm GEMMs in the pipelined graph (0 = all; default: "
                          "80 for the training step, measured best of 48..148, 0 for inference)")
@@ -885,12 +1109,23 @@ def main():
     if args.norm_sms < 0:   # measured: the budget helps the C2 training pipeline only
         args.norm_sms = 104 if (args.mode == "train" and args.config == "c2") else 0
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: re-exec under torchrun, one rank per
+        # GPU (the driver's own N > 1 command already runs under torchrun)
+        sys.exit(self_launch(args.gpus))
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}",
+              file=sys.stderr, flush=True)
     dist = None
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.stub:
+        run_stub(args, rank, world)
         return
     if world > 1:
         import torch
@@ -900,10 +1135,54 @@ def main():
         dist = tdist
     if args.config == "c5":
         run_stack(args, rank, world, local_rank, dist)
+    elif args.mode == "dsplit":
+        run_dsplit(args, rank, world, local_rank, dist)
     else:
         run_gpu(args, rank, world, local_rank, dist)
     if dist:
         dist.destroy_process_group()
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(n: int) -> int:
+    """Run this same command as n ranks under torch.distributed.run (127.0.0.1 rendezvous)."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_stub(args, rank, world):
+    """Launcher check without a GPU (tests/test_bench_contract.py): the same rendezvous, barrier
+    and max-over-ranks reduction as the GPU arm on gloo, a trivial CPU 'step', and rank 0's
+    JSON line with the whole-job fields.  Never a bench number."""
+    import torch
+    import torch.distributed as tdist
+    if world > 1:
+        tdist.init_process_group("gloo")
+    t0 = time.perf_counter()
+    x = torch.ones(1024)
+    for _ in range(args.steps):
+        x = x * 1.0
+    ms = (time.perf_counter() - t0) * 1e3
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        tdist.barrier()
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({"stub": True, "metric": METRIC, "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "value": world * args.steps / max(ms / 1e3, 1e-9),
+                          "ranks_reporting": world}), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
 
 
 if __name__ == "__main__":

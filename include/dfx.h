@@ -198,6 +198,39 @@ int dfx_module_train_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const vo
                           int64_t rows, int64_t chunk_size, void* delta, void* d_lora,
                           void* d_base, float* d_mag, float* g);
 
+/* ---- Symmetric-memory all-reduce for the d_in-split norm ----
+ * The exchange between dfx_norm_partial and dfx_norm_finish as one kernel
+ * over peer memory instead of a library collective.  Each rank creates a comm whose symmetric
+ * allocation holds `count` fp32 (count >= r*r + 2*d_out); the ranks exchange their IPC handles
+ * out of band (e.g. torch.distributed all_gather_object) and open them (ranks that share a
+ * process pass each other's bases with dfx_comm_set_peers instead).  The rank writes its
+ * partial terms into dfx_comm_buffer(); dfx_norm_allreduce then writes
+ *     out[i] = ((buf_0[i] + buf_1[i]) + buf_2[i]) + ...      (rank order, fp32, RN)
+ * on every rank — identical bits on every rank — with an entry and an exit barrier over
+ * device flags (no host synchronisation; capturable in a CUDA graph).  Every rank must issue
+ * the same sequence of dfx_norm_allreduce calls.  Spins are bounded (~5 s): a missing peer
+ * raises the comm's error word (dfx_comm_status) rather than hanging the device. */
+typedef struct dfx_comm dfx_comm;
+#define DFX_IPC_HANDLE_BYTES 64
+int dfx_comm_create(dfx_ctx* ctx, int rank, int world, int64_t count, dfx_comm** out);
+void dfx_comm_destroy(dfx_comm* comm);
+/* This rank's symmetric data region [count fp32] (device pointer). */
+float* dfx_comm_buffer(dfx_comm* comm);
+/* Base of this rank's symmetric allocation (what peers in the same process map). */
+void* dfx_comm_base(dfx_comm* comm);
+/* cudaIpcMemHandle_t of this rank's allocation (DFX_IPC_HANDLE_BYTES bytes into `out`). */
+int dfx_comm_ipc_handle(dfx_comm* comm, void* out);
+/* Open the peers' allocations: `handles` = world * DFX_IPC_HANDLE_BYTES bytes in rank order
+ * (this rank's own entry is ignored). */
+int dfx_comm_open(dfx_comm* comm, const void* handles);
+/* Same-process peers: bases[k] = dfx_comm_base of rank k's comm (bases[rank] ignored). */
+int dfx_comm_set_peers(dfx_comm* comm, void* const* bases);
+/* out [count] = rank-order sum of every rank's dfx_comm_buffer (stream-ordered). */
+int dfx_norm_allreduce(dfx_comm* comm, float* out, int64_t count, dfx_stream_t stream);
+/* *timed_out = 0 when every barrier so far completed, 1 when a spin timed out (a peer never
+ * arrived; the results of that call are invalid).  Synchronises with the comm's device. */
+int dfx_comm_status(dfx_comm* comm, int* timed_out);
+
 /* The bf16 tensor-core norm's plan for this shape under the context's SM budget
  * (dfx_ctx_set_sm_budget): SMs the W.A^T kernel occupies, SMs given to the Gram / V
  * kernels on the side stream (0 when they run after it), strategy (0 Gram and V beside

@@ -26,14 +26,18 @@ struct Workspace {
     int device = 0;
     int sms = 0;
     int sm_budget = 0;      // dfx_ctx_set_sm_budget: cap on the SMs the norm's GEMMs plan for
+    cudaStream_t cur = nullptr;     // the calling entry point's stream (capture check)
+    bool grow_in_capture = false;   // a call needed to grow the workspace during capture
     std::vector<void*> ptr;
     std::vector<size_t> cap;
+    std::vector<void*> retired;     // outgrown buffers: freed at dfx_ctx_destroy only
     cudaStream_t side = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     Workspace() : ptr(16, nullptr), cap(16, 0) {}
     ~Workspace() {
         for (void* p : ptr)
             if (p) cudaFree(p);
+        for (void* p : retired) cudaFree(p);
         for (cudaEvent_t e : ev)
             if (e) cudaEventDestroy(e);
         if (side) cudaStreamDestroy(side);
@@ -54,37 +58,66 @@ cudaEvent_t ws_event(Workspace* ws, int idx, cudaError_t* err) {
     return ws->ev[idx];
 }
 
+int device_sm_count() {
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (!cache[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = v > 0 ? v : 148;
+    }
+    return cache[dev];
+}
+
+int device_smem_optin() {
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 227 * 1024;
+    if (!cache[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cache[dev] = v > 0 ? v : 227 * 1024;
+    }
+    return cache[dev];
+}
+
 int ws_sm_count(Workspace* ws) {
     if (!ws->sms) cudaDeviceGetAttribute(&ws->sms, cudaDevAttrMultiProcessorCount, ws->device);
     const int n = ws->sms > 0 ? ws->sms : 148;
     return ws->sm_budget > 0 ? std::min(n, std::max(ws->sm_budget, 4)) : n;
 }
 
+// Grow-only workspace slots.  Growth never synchronises and never frees: the outgrown buffer
+// may still be read by queued work on any stream or be baked into a CUDA graph captured
+// earlier, so it is retired and freed only by dfx_ctx_destroy.  Growth is refused (the call
+// fails with DFX_EUNSUPPORTED) while the calling stream is capturing a graph: run the call
+// once eagerly at the largest shape first.
 void* ws_get(Workspace* ws, int slot, size_t bytes, cudaError_t* err) {
     *err = cudaSuccess;
     if (bytes == 0) bytes = 16;
     if (ws->cap[slot] >= bytes) return ws->ptr[slot];
-    if (ws->ptr[slot]) {
-        // the old buffer may still be read by queued work on any stream
-        cudaDeviceSynchronize();
-        cudaFree(ws->ptr[slot]);
-        ws->ptr[slot] = nullptr;
-        ws->cap[slot] = 0;
-    }
-    const size_t want = bytes + bytes / 4;
-    *err = cudaMalloc(&ws->ptr[slot], want);
-    if (*err != cudaSuccess) {
-        ws->ptr[slot] = nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(ws->cur, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        ws->grow_in_capture = true;
+        *err = cudaErrorStreamCaptureUnsupported;
         return nullptr;
     }
+    const size_t want = bytes + bytes / 4;
+    void* p = nullptr;
+    *err = cudaMalloc(&p, want);
+    if (*err != cudaSuccess) return nullptr;
+    if (ws->ptr[slot]) ws->retired.push_back(ws->ptr[slot]);
+    ws->ptr[slot] = p;
     ws->cap[slot] = want;
-    return ws->ptr[slot];
+    return p;
 }
 
 void* ws_get_zeroed(Workspace* ws, int slot, size_t bytes, cudaError_t* err) {
     const bool fresh = ws->cap[slot] < (bytes ? bytes : 16);
     void* p = ws_get(ws, slot, bytes, err);
-    if (*err == cudaSuccess && fresh) *err = cudaMemset(p, 0, ws->cap[slot]);
+    if (*err == cudaSuccess && fresh) *err = cudaMemsetAsync(p, 0, ws->cap[slot], ws->cur);
     return p;
 }
 
@@ -208,6 +241,7 @@ struct dfx_ctx {
     cudaStream_t st_h2d = nullptr, st_comp = nullptr, st_d2h = nullptr;
     std::vector<void*> stage;
     std::vector<size_t> stage_cap;
+    std::vector<void*> stage_retired;
 };
 
 namespace {
@@ -230,16 +264,52 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 bool valid_dtype(int dt) { return dt == DFX_F32 || dt == DFX_BF16 || dt == DFX_F16; }
 
-// Binds the calling thread to the context's device (and its profiler, if enabled).
-int enter(dfx_ctx* ctx) {
+// Restores the caller's current device when an entry point returns (the host framework's
+// device state is not ours to change).
+struct DeviceGuard {
+    int prev = -1;
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// Binds the calling thread to the context's device (restored by `dg` on return), records the
+// call's stream for the workspace's capture check, checks that the stream belongs to the
+// context's device, and attaches the context's profiler if enabled.
+int enter(dfx_ctx* ctx, DeviceGuard& dg, cudaStream_t st = nullptr) {
     if (!ctx) return fail(DFX_EINVAL, "null context");
-    const cudaError_t e = cudaSetDevice(ctx->device);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    int cur = -1;
+    cudaError_t e = cudaGetDevice(&cur);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (cur != ctx->device) {
+        e = cudaSetDevice(ctx->device);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+        dg.prev = cur;
+    }
+#if CUDART_VERSION >= 12080
+    // (outside graph capture only: the query is not a capturable call)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (st && cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+        int sdev = -1;
+        if (cudaStreamGetDevice(st, &sdev) == cudaSuccess && sdev != ctx->device)
+            return fail(DFX_EINVAL, "stream belongs to device %d, context to device %d", sdev,
+                        ctx->device);
+        cudaGetLastError();
+    }
+#endif
+    ctx->ws.cur = st;
+    ctx->ws.grow_in_capture = false;
     dfx::g_prof = ctx->profiling ? &ctx->prof : nullptr;
     return DFX_OK;
 }
 
-int finish_call(cudaError_t e, const char* where) {
+int finish_call(dfx_ctx* ctx, cudaError_t e, const char* where) {
+    if (e != cudaSuccess && ctx && ctx->ws.grow_in_capture) {
+        cudaGetLastError();
+        return fail(DFX_EUNSUPPORTED,
+                    "%s: the workspace must grow for this shape/plan but the stream is capturing "
+                    "a graph; call once eagerly first", where);
+    }
     if (e != cudaSuccess) return cuda_fail(e, where);
     g_err.clear();
     return DFX_OK;
@@ -268,8 +338,6 @@ int dfx_ctx_create(int device, dfx_ctx** out) {
     if (prop.major != 10 || prop.minor != 0)
         return fail(DFX_ENODEV, "dfx: built for sm_100a, device %d is sm_%d%d", device, prop.major,
                     prop.minor);
-    e = cudaSetDevice(device);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
     dfx_ctx* c = new dfx_ctx();
     c->device = device;
     c->ws.device = device;
@@ -282,10 +350,16 @@ int dfx_ctx_create(int device, dfx_ctx** out) {
 
 void dfx_ctx_destroy(dfx_ctx* ctx) {
     if (!ctx) return;
-    cudaSetDevice(ctx->device);
+    DeviceGuard dg;
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != ctx->device) {
+        cudaSetDevice(ctx->device);
+        dg.prev = cur;
+    }
     cudaDeviceSynchronize();
     for (void* p : ctx->stage)
         if (p) cudaFree(p);
+    for (void* p : ctx->stage_retired) cudaFree(p);
     if (ctx->st_h2d) cudaStreamDestroy(ctx->st_h2d);
     if (ctx->st_comp) cudaStreamDestroy(ctx->st_comp);
     if (ctx->st_d2h) cudaStreamDestroy(ctx->st_d2h);
@@ -303,7 +377,8 @@ int dfx_profile_enable(dfx_ctx* ctx, int on) {
 }
 
 int dfx_profile_report(dfx_ctx* ctx, char* buf, size_t len) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg);
     if (rc) return rc;
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e, "dfx_profile_report");
@@ -371,11 +446,12 @@ int dfx_plan_chunks(uint64_t d_out, uint64_t d_in, uint64_t budget, uint64_t* ch
 
 int dfx_norm_plan(dfx_ctx* ctx, dfx_dtype dtype, int64_t d_out, int64_t d_in, int64_t r,
                   int64_t chunk_size, int* u_sms, int* side_sms, int* strategy) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg);
     if (rc) return rc;
-    if (dtype != DFX_BF16 || chunk_size <= 0 || chunk_size % 64 != 0 ||
+    if ((dtype != DFX_BF16 && dtype != DFX_F16) || chunk_size <= 0 || chunk_size % 64 != 0 ||
         !dfx::norm_uses_tensor_cores(dtype, d_out, d_in, r))
-        return fail(DFX_EUNSUPPORTED, "dfx_norm_plan: not the bf16 tensor-core path");
+        return fail(DFX_EUNSUPPORTED, "dfx_norm_plan: not the bf16 / fp16 tensor-core path");
     dfx::norm_plan_info(d_out, d_in, r, chunk_size, dfx::ws_sm_count(&ctx->ws), u_sms, side_sms,
                         strategy);
     return DFX_OK;
@@ -412,13 +488,14 @@ static int run_norm(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A,
     int launches = 0;
     const cudaError_t e = dfx::launch_norm(a, &ctx->ws, st, &launches);
     ctx->launches += launches;
-    return finish_call(e, where);
+    return finish_call(ctx, e, where);
 }
 
 int dfx_norm_terms(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A, const void* B,
                    int64_t d_out, int64_t d_in, int64_t r, double s, int64_t chunk_size,
                    float* base_sq, float* cross, float* ba_sq, dfx_stream_t stream) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
     if (rc) return rc;
     rc = check_norm_args(dtype, W, A, B, d_out, d_in, r, chunk_size);
     if (rc) return rc;
@@ -430,7 +507,8 @@ int dfx_row_norm(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A, co
                  int64_t d_out, int64_t d_in, int64_t r, double s, int64_t chunk_size,
                  const float* m, dfx_dtype mag_dtype, float* w_norm, float* g, float* terms,
                  dfx_stream_t stream) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
     if (rc) return rc;
     rc = check_norm_args(dtype, W, A, B, d_out, d_in, r, chunk_size);
     if (rc) return rc;
@@ -447,7 +525,8 @@ int dfx_row_norm_cached(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void
                         const void* B, int64_t d_out, int64_t d_in, int64_t r, double s,
                         int64_t chunk_size, float* base_sq_cache, int refresh, const float* m,
                         dfx_dtype mag_dtype, float* w_norm, float* g, dfx_stream_t stream) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
     if (rc) return rc;
     rc = check_norm_args(dtype, W, A, B, d_out, d_in, r, chunk_size);
     if (rc) return rc;
@@ -469,13 +548,14 @@ int dfx_row_norm_cached(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void
     int launches = 0;
     const cudaError_t e = dfx::launch_norm(a, &ctx->ws, stream, &launches);
     ctx->launches += launches;
-    return finish_call(e, "dfx_row_norm_cached");
+    return finish_call(ctx, e, "dfx_row_norm_cached");
 }
 
 int dfx_norm_partial(dfx_ctx* ctx, dfx_dtype dtype, const void* W_k, const void* A_k,
                      const void* B, int64_t d_out, int64_t d_in_k, int64_t r, int64_t chunk_size,
                      float* gram, float* base_sq, float* cross, dfx_stream_t stream) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
     if (rc) return rc;
     rc = check_norm_args(dtype, W_k, A_k, B, d_out, d_in_k, r, chunk_size);
     if (rc) return rc;
@@ -490,14 +570,15 @@ int dfx_norm_partial(dfx_ctx* ctx, dfx_dtype dtype, const void* W_k, const void*
     int launches = 0;
     const cudaError_t e = dfx::launch_norm(a, &ctx->ws, stream, &launches);
     ctx->launches += launches;
-    return finish_call(e, "dfx_norm_partial");
+    return finish_call(ctx, e, "dfx_norm_partial");
 }
 
 int dfx_norm_finish(dfx_ctx* ctx, dfx_dtype dtype, const void* B, const float* gram,
                     const float* base_sq, const float* cross, int64_t d_out, int64_t r, double s,
                     const float* m, dfx_dtype mag_dtype, float* w_norm, float* g, float* terms,
                     dfx_stream_t stream) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
     if (rc) return rc;
     if (!valid_dtype(dtype)) return fail(DFX_EINVAL, "dfx_norm_finish: dtype");
     if (d_out < 0 || r < 1) return fail(DFX_EINVAL, "factored_norm: rank must be >= 1");
@@ -515,13 +596,14 @@ int dfx_norm_finish(dfx_ctx* ctx, dfx_dtype dtype, const void* B, const float* g
     int launches = 0;
     const cudaError_t e = dfx::launch_norm(a, &ctx->ws, stream, &launches);
     ctx->launches += launches;
-    return finish_call(e, "dfx_norm_finish");
+    return finish_call(ctx, e, "dfx_norm_finish");
 }
 
 int dfx_assemble_norm(dfx_ctx* ctx, const float* base_sq, const float* cross,
                       const float* ba_sq, double two_s, double s2, int64_t n,
                       dfx_dtype round_to, float* w_norm, dfx_stream_t stream) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
     if (rc) return rc;
     if (n < 0) return fail(DFX_EINVAL, "assemble_norm: term vectors differ in length");
     if (!valid_dtype(round_to)) return fail(DFX_EUNSUPPORTED, "assemble_norm: dtype");
@@ -531,12 +613,13 @@ int dfx_assemble_norm(dfx_ctx* ctx, const float* base_sq, const float* cross,
     const cudaError_t e = dfx::launch_assemble(base_sq, cross, ba_sq, two_s, s2, n, round_to,
                                                w_norm, stream, &launches);
     ctx->launches += launches;
-    return finish_call(e, "dfx_assemble_norm");
+    return finish_call(ctx, e, "dfx_assemble_norm");
 }
 
 int dfx_magnitude_scale(dfx_ctx* ctx, dfx_dtype dtype, const float* m, const float* w_norm,
                         int64_t n, float* g, dfx_stream_t stream) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
     if (rc) return rc;
     if (!valid_dtype(dtype)) return fail(DFX_EUNSUPPORTED, "magnitude_scale: fp64 is host-only");
     if (n < 0) return fail(DFX_EINVAL, "magnitude_scale: length mismatch");
@@ -544,13 +627,14 @@ int dfx_magnitude_scale(dfx_ctx* ctx, dfx_dtype dtype, const float* m, const flo
     int launches = 0;
     const cudaError_t e = dfx::launch_magnitude_scale(dtype, m, w_norm, n, g, stream, &launches);
     ctx->launches += launches;
-    return finish_call(e, "dfx_magnitude_scale");
+    return finish_call(ctx, e, "dfx_magnitude_scale");
 }
 
 int dfx_compose_fwd(dfx_ctx* ctx, dfx_dtype dtype, const void* base, const void* lora,
                     const float* g, double s, int64_t rows, int64_t d_out, void* delta,
                     void* inner, dfx_stream_t stream) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
     if (rc) return rc;
     if (!valid_dtype(dtype)) return fail(DFX_EUNSUPPORTED, "compose: dtype");
     if (rows < 0 || d_out < 0) return fail(DFX_EINVAL, "compose: base/lora shapes differ");
@@ -561,13 +645,14 @@ int dfx_compose_fwd(dfx_ctx* ctx, dfx_dtype dtype, const void* base, const void*
         dfx::launch_compose_fwd(dtype, base, lora, g, static_cast<float>(s), rows, d_out, delta,
                                 inner, stream, &launches);
     ctx->launches += launches;
-    return finish_call(e, "dfx_compose_fwd");
+    return finish_call(ctx, e, "dfx_compose_fwd");
 }
 
 int dfx_compose_bwd(dfx_ctx* ctx, dfx_dtype dtype, const void* dy, const float* g, double s,
                     const void* inner, const float* w_norm, int64_t rows, int64_t d_out,
                     void* d_lora, void* d_base, float* d_mag, dfx_stream_t stream) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
     if (rc) return rc;
     if (!valid_dtype(dtype)) return fail(DFX_EUNSUPPORTED, "compose_backward: dtype");
     if (rows < 0 || d_out < 0) return fail(DFX_EINVAL, "compose_backward: g length != d_out");
@@ -584,23 +669,78 @@ int dfx_compose_bwd(dfx_ctx* ctx, dfx_dtype dtype, const void* dy, const float* 
         dfx::launch_compose_bwd(dtype, dy, g, static_cast<float>(s), inner, w_norm, rows, d_out,
                                 d_lora, d_base, d_mag, stream, &launches, ctx->ws.sm_budget > 0);
     ctx->launches += launches;
-    return finish_call(e, "dfx_compose_bwd");
+    return finish_call(ctx, e, "dfx_compose_bwd");
 }
 
+// Host-entry staging buffers (grow-only).  An outgrown buffer is retired, not freed: freeing
+// would synchronise the device; the retired ones are released by dfx_ctx_destroy.
 static void* stage_buf(dfx_ctx* ctx, int slot, size_t bytes, cudaError_t* e) {
     *e = cudaSuccess;
     if (bytes == 0) bytes = 16;
     if (ctx->stage_cap[slot] >= bytes) return ctx->stage[slot];
-    if (ctx->stage[slot]) {
-        cudaDeviceSynchronize();
-        cudaFree(ctx->stage[slot]);
-    }
-    ctx->stage[slot] = nullptr;
-    ctx->stage_cap[slot] = 0;
-    *e = cudaMalloc(&ctx->stage[slot], bytes);
+    void* p = nullptr;
+    *e = cudaMalloc(&p, bytes);
     if (*e != cudaSuccess) return nullptr;
+    if (ctx->stage[slot]) ctx->stage_retired.push_back(ctx->stage[slot]);
+    ctx->stage[slot] = p;
     ctx->stage_cap[slot] = bytes;
-    return ctx->stage[slot];
+    return p;
+}
+
+// One blocking host-buffer call: records the first failing CUDA call and, however the call
+// ends (success or any error path), waits for all three staging streams before returning, so
+// no DMA into or out of the caller's host buffers is in flight afterwards, then releases the
+// call's events.
+struct HostCall {
+    dfx_ctx* c;
+    std::vector<cudaEvent_t> evs;
+    cudaError_t first = cudaSuccess;
+    const char* where = "";
+    explicit HostCall(dfx_ctx* ctx) : c(ctx) {}
+    bool ok(cudaError_t e, const char* w) {
+        if (e != cudaSuccess && first == cudaSuccess) {
+            first = e;
+            where = w;
+        }
+        return first == cudaSuccess;
+    }
+    cudaEvent_t event() {
+        cudaEvent_t ev = nullptr;
+        if (ok(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate"))
+            evs.push_back(ev);
+        return ev;
+    }
+    // stream `to` waits for the work queued so far on `from`
+    bool link(cudaStream_t from, cudaStream_t to) {
+        cudaEvent_t ev = event();
+        return ok(ev ? cudaEventRecord(ev, from) : first, "cudaEventRecord") &&
+               ok(cudaStreamWaitEvent(to, ev, 0), "cudaStreamWaitEvent");
+    }
+    bool copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
+        return ok(cudaMemcpyAsync(dst, src, bytes, kind, st), "cudaMemcpyAsync");
+    }
+    cudaError_t drain() {
+        const cudaError_t a = cudaStreamSynchronize(c->st_h2d);
+        const cudaError_t b = cudaStreamSynchronize(c->st_comp);
+        const cudaError_t d = cudaStreamSynchronize(c->st_d2h);
+        return a != cudaSuccess ? a : b != cudaSuccess ? b : d;
+    }
+    ~HostCall() {
+        if (c->st_h2d) drain();
+        for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+    }
+};
+
+static int host_streams(dfx_ctx* ctx) {
+    cudaError_t e = cudaSuccess;
+    if (!ctx->st_h2d) {
+        if ((e = cudaStreamCreateWithFlags(&ctx->st_h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&ctx->st_comp, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&ctx->st_d2h, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e, "stream create");
+    }
+    ctx->ws.cur = ctx->st_comp;
+    return DFX_OK;
 }
 
 int dfx_ctx_set_sm_budget(dfx_ctx* ctx, int sms) {
@@ -613,7 +753,8 @@ int dfx_ctx_set_sm_budget(dfx_ctx* ctx, int sms) {
 int dfx_working_matmul(dfx_ctx* ctx, dfx_dtype dtype, const void* A, int64_t sa_i, int64_t sa_k,
                        const void* B, int64_t sb_k, int64_t sb_j, int64_t M, int64_t N, int64_t K,
                        void* C, dfx_stream_t stream) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
     if (rc) return rc;
     if (!valid_dtype(dtype)) return fail(DFX_EUNSUPPORTED, "working_matmul: dtype");
     if (M < 0 || N < 0 || K < 0) return fail(DFX_EINVAL, "working_matmul: negative dimension");
@@ -623,14 +764,15 @@ int dfx_working_matmul(dfx_ctx* ctx, dfx_dtype dtype, const void* A, int64_t sa_
     const cudaError_t e = dfx::launch_working_matmul(dtype, A, sa_i, sa_k, B, sb_k, sb_j, M, N, K, C,
                                                      stream, &launches);
     ctx->launches += launches;
-    return finish_call(e, "dfx_working_matmul");
+    return finish_call(ctx, e, "dfx_working_matmul");
 }
 
 int dfx_lora_compose(dfx_ctx* ctx, dfx_dtype dtype, const void* mid, const void* B,
                      const void* base, const float* g, double s, const float* bias, int64_t rows,
                      int64_t d_out, int64_t r, void* y, void* delta, void* inner, void* lora,
                      dfx_stream_t stream) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
     if (rc) return rc;
     if (dtype != DFX_BF16 && dtype != DFX_F16)
         return fail(DFX_EUNSUPPORTED, "lora_compose: bf16 / fp16 only (tcgen05 kind::f16)");
@@ -654,101 +796,231 @@ int dfx_lora_compose(dfx_ctx* ctx, dfx_dtype dtype, const void* mid, const void*
                                                    bias, rows, d_out, r, y, delta, inner, lora,
                                                    stream, &launches);
     ctx->launches += launches;
-    return finish_call(e, "dfx_lora_compose");
+    return finish_call(ctx, e, "dfx_lora_compose");
+}
+
+// ------------------------------------------------------- symmetric-memory all-reduce
+}  // extern "C"
+
+struct dfx_comm {
+    dfx_ctx* ctx = nullptr;
+    int rank = 0, world = 1;
+    int64_t count = 0;
+    char* base = nullptr;
+    size_t bytes = 0;
+    dfx::CommArgs args{};
+    std::vector<void*> opened;   // peer bases mapped through CUDA IPC (closed at destroy)
+    bool ready = false;
+};
+
+extern "C" {
+
+int dfx_comm_create(dfx_ctx* ctx, int rank, int world, int64_t count, dfx_comm** out) {
+    DeviceGuard dg;
+    int rc = enter(ctx, dg);
+    if (rc) return rc;
+    if (!out) return fail(DFX_EINVAL, "dfx_comm_create: null out");
+    *out = nullptr;
+    if (world < 1 || world > dfx::kCommMaxRanks || rank < 0 || rank >= world)
+        return fail(DFX_EINVAL, "dfx_comm_create: rank %d of world %d (max %d ranks)", rank, world,
+                    dfx::kCommMaxRanks);
+    if (count < 0) return fail(DFX_EINVAL, "dfx_comm_create: negative count");
+    const size_t data = (size_t(count) * 4 + 255) / 256 * 256;
+    const size_t flags = size_t(dfx::kCommMaxBlocks) * dfx::kCommMaxRanks * 4;
+    dfx_comm* c = new dfx_comm();
+    c->ctx = ctx;
+    c->rank = rank;
+    c->world = world;
+    c->count = count;
+    c->args.rank = rank;
+    c->args.world = world;
+    c->args.start_off = data;
+    c->args.end_off = data + flags;
+    c->args.epoch_off = data + 2 * flags;
+    c->args.err_off = c->args.epoch_off + dfx::kCommMaxBlocks * 4;
+    c->bytes = c->args.err_off + 256;
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, c->bytes);
+    if (e == cudaSuccess) e = cudaMemset(p, 0, c->bytes);   // flags, epochs, error word = 0
+    if (e != cudaSuccess) {
+        if (p) cudaFree(p);
+        delete c;
+        return cuda_fail(e, "dfx_comm_create");
+    }
+    c->base = static_cast<char*>(p);
+    c->args.peers[rank] = c->base;
+    c->ready = world == 1;
+    *out = c;
+    g_err.clear();
+    return DFX_OK;
+}
+
+void dfx_comm_destroy(dfx_comm* comm) {
+    if (!comm) return;
+    DeviceGuard dg;
+    if (enter(comm->ctx, dg) == DFX_OK) {
+        cudaDeviceSynchronize();
+        for (void* p : comm->opened) cudaIpcCloseMemHandle(p);
+        if (comm->base) cudaFree(comm->base);
+    }
+    delete comm;
+}
+
+float* dfx_comm_buffer(dfx_comm* comm) {
+    return comm ? reinterpret_cast<float*>(comm->base) : nullptr;
+}
+
+void* dfx_comm_base(dfx_comm* comm) { return comm ? comm->base : nullptr; }
+
+int dfx_comm_ipc_handle(dfx_comm* comm, void* out) {
+    if (!comm || !out) return fail(DFX_EINVAL, "dfx_comm_ipc_handle: null argument");
+    DeviceGuard dg;
+    int rc = enter(comm->ctx, dg);
+    if (rc) return rc;
+    static_assert(sizeof(cudaIpcMemHandle_t) == DFX_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, comm->base);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    std::memcpy(out, &h, sizeof(h));
+    g_err.clear();
+    return DFX_OK;
+}
+
+int dfx_comm_open(dfx_comm* comm, const void* handles) {
+    if (!comm || !handles) return fail(DFX_EINVAL, "dfx_comm_open: null argument");
+    DeviceGuard dg;
+    int rc = enter(comm->ctx, dg);
+    if (rc) return rc;
+    if (comm->ready && comm->world > 1) return fail(DFX_EINVAL, "dfx_comm_open: peers already set");
+    for (int k = 0; k < comm->world; ++k) {
+        if (k == comm->rank) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const char*>(handles) + size_t(k) * sizeof(h), sizeof(h));
+        void* p = nullptr;
+        const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+        comm->opened.push_back(p);
+        comm->args.peers[k] = static_cast<char*>(p);
+    }
+    comm->ready = true;
+    g_err.clear();
+    return DFX_OK;
+}
+
+int dfx_comm_set_peers(dfx_comm* comm, void* const* bases) {
+    if (!comm || !bases) return fail(DFX_EINVAL, "dfx_comm_set_peers: null argument");
+    for (int k = 0; k < comm->world; ++k) {
+        if (k == comm->rank) continue;
+        if (!bases[k]) return fail(DFX_EINVAL, "dfx_comm_set_peers: null base for rank %d", k);
+        comm->args.peers[k] = static_cast<char*>(bases[k]);
+    }
+    comm->ready = true;
+    g_err.clear();
+    return DFX_OK;
+}
+
+int dfx_norm_allreduce(dfx_comm* comm, float* out, int64_t count, dfx_stream_t stream) {
+    if (!comm) return fail(DFX_EINVAL, "dfx_norm_allreduce: null comm");
+    dfx_ctx* ctx = comm->ctx;
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
+    if (rc) return rc;
+    if (!comm->ready) return fail(DFX_EINVAL, "dfx_norm_allreduce: peers not opened");
+    if (count < 0 || count > comm->count)
+        return fail(DFX_EINVAL, "dfx_norm_allreduce: count %lld outside the symmetric buffer (%lld)",
+                    (long long)count, (long long)comm->count);
+    if (count > 0 && !out) return fail(DFX_EINVAL, "dfx_norm_allreduce: null out");
+    dfx::CommArgs a = comm->args;
+    a.count = count;
+    a.out = out;
+    const int64_t n4 = (count + 3) / 4;
+    a.max_blocks = static_cast<int>(std::min<int64_t>(
+        dfx::kCommMaxBlocks, std::max<int64_t>(1, (n4 + dfx::kCommThreads - 1) / dfx::kCommThreads)));
+    int launches = 0;
+    const cudaError_t e = dfx::launch_allreduce(a, stream, &launches);
+    ctx->launches += launches;
+    return finish_call(ctx, e, "dfx_norm_allreduce");
+}
+
+int dfx_comm_status(dfx_comm* comm, int* timed_out) {
+    if (!comm || !timed_out) return fail(DFX_EINVAL, "dfx_comm_status: null argument");
+    DeviceGuard dg;
+    int rc = enter(comm->ctx, dg);
+    if (rc) return rc;
+    uint32_t err = 0;
+    const cudaError_t e = cudaMemcpy(&err, comm->base + comm->args.err_off, 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "dfx_comm_status");
+    *timed_out = err ? 1 : 0;
+    g_err.clear();
+    return DFX_OK;
 }
 
 int dfx_module_fwd_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A,
                         const void* B, const float* m, const void* base, const void* lora,
                         double s, int64_t d_out, int64_t d_in, int64_t r, int64_t rows,
                         int64_t chunk_size, void* delta, float* g) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg);
     if (rc) return rc;
     rc = check_norm_args(dtype, W, A, B, d_out, d_in, r, chunk_size);
     if (rc) return rc;
     if (rows < 0 || !m || !g || (rows > 0 && (!base || !lora || !delta)))
         return fail(DFX_EINVAL, "dfx_module_fwd_host: null operand");
-    cudaError_t e = cudaSuccess;
-    if (!ctx->st_h2d) {
-        if ((e = cudaStreamCreateWithFlags(&ctx->st_h2d, cudaStreamNonBlocking)) != cudaSuccess ||
-            (e = cudaStreamCreateWithFlags(&ctx->st_comp, cudaStreamNonBlocking)) != cudaSuccess ||
-            (e = cudaStreamCreateWithFlags(&ctx->st_d2h, cudaStreamNonBlocking)) != cudaSuccess)
-            return cuda_fail(e, "stream create");
-    }
+    if ((rc = host_streams(ctx))) return rc;
     const size_t eb = dtype == DFX_F32 ? 4 : 2;
     const size_t nW = size_t(d_out) * d_in, nA = size_t(r) * d_in, nB = size_t(d_out) * r;
     const size_t nact = size_t(rows) * d_out;
-    void* dW = stage_buf(ctx, 0, nW * eb, &e);
-    if (e) return cuda_fail(e, "stage alloc");
-    void* dA = stage_buf(ctx, 1, nA * eb, &e);
-    if (e) return cuda_fail(e, "stage alloc");
-    void* dB = stage_buf(ctx, 2, nB * eb, &e);
-    if (e) return cuda_fail(e, "stage alloc");
-    float* dm = static_cast<float*>(stage_buf(ctx, 3, d_out * 4, &e));
-    if (e) return cuda_fail(e, "stage alloc");
-    float* dg = static_cast<float*>(stage_buf(ctx, 4, d_out * 4, &e));
-    if (e) return cuda_fail(e, "stage alloc");
-    float* dwn = static_cast<float*>(stage_buf(ctx, 5, d_out * 4, &e));
-    if (e) return cuda_fail(e, "stage alloc");
-    void* dbase = stage_buf(ctx, 6, nact * eb, &e);
-    if (e) return cuda_fail(e, "stage alloc");
-    void* dlora = stage_buf(ctx, 7, nact * eb, &e);
-    if (e) return cuda_fail(e, "stage alloc");
-    void* ddelta = stage_buf(ctx, 8, nact * eb, &e);
-    if (e) return cuda_fail(e, "stage alloc");
+    const size_t sizes[9] = {nW * eb, nA * eb, nB * eb, size_t(d_out) * 4, size_t(d_out) * 4,
+                             size_t(d_out) * 4, nact * eb, nact * eb, nact * eb};
+    void* buf[9];
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 9; ++i) {
+        buf[i] = stage_buf(ctx, i, sizes[i], &e);
+        if (e) return cuda_fail(e, "stage alloc");
+    }
+    void *dW = buf[0], *dA = buf[1], *dB = buf[2];
+    float *dm = static_cast<float*>(buf[3]), *dg_ = static_cast<float*>(buf[4]);
+    float* dwn = static_cast<float*>(buf[5]);
+    void *dbase = buf[6], *dlora = buf[7], *ddelta = buf[8];
 
-    cudaEvent_t ev_norm, ev_w;
-    cudaEventCreateWithFlags(&ev_norm, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_w, cudaEventDisableTiming);
+    HostCall hc(ctx);
     // weights first: the norm overlaps the activation upload
-    cudaMemcpyAsync(dA, A, nA * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
-    cudaMemcpyAsync(dB, B, nB * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
-    cudaMemcpyAsync(dm, m, d_out * 4, cudaMemcpyHostToDevice, ctx->st_h2d);
-    cudaMemcpyAsync(dW, W, nW * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
-    cudaEventRecord(ev_w, ctx->st_h2d);
-    cudaStreamWaitEvent(ctx->st_comp, ev_w, 0);
+    hc.copy(dA, A, nA * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
+    hc.copy(dB, B, nB * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
+    hc.copy(dm, m, d_out * 4, cudaMemcpyHostToDevice, ctx->st_h2d);
+    hc.copy(dW, W, nW * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
+    if (!hc.link(ctx->st_h2d, ctx->st_comp)) return cuda_fail(hc.first, hc.where);
     rc = run_norm(ctx, dtype, dW, dA, dB, d_out, d_in, r, s, chunk_size, nullptr, nullptr,
-                  nullptr, dm, dtype, dwn, dg, dtype, ctx->st_comp, "dfx_module_fwd_host/norm");
+                  nullptr, dm, dtype, dwn, dg_, dtype, ctx->st_comp, "dfx_module_fwd_host/norm");
     if (rc) return rc;
-    cudaEventRecord(ev_norm, ctx->st_comp);
-    cudaStreamWaitEvent(ctx->st_d2h, ev_norm, 0);
-    cudaMemcpyAsync(g, dg, d_out * 4, cudaMemcpyDeviceToHost, ctx->st_d2h);
+    if (!hc.link(ctx->st_comp, ctx->st_d2h) ||
+        !hc.copy(g, dg_, d_out * 4, cudaMemcpyDeviceToHost, ctx->st_d2h))
+        return cuda_fail(hc.first, hc.where);
 
     // activations in row chunks: upload chunk c+1 while composing c and downloading c-1
     const int64_t nchunk = rows >= 1024 ? 8 : 1;
-    const int64_t crow = (rows + nchunk - 1) / nchunk;
-    std::vector<cudaEvent_t> evs;
+    const int64_t crow = rows > 0 ? (rows + nchunk - 1) / nchunk : 1;
     for (int64_t r0 = 0; r0 < rows; r0 += crow) {
         const int64_t nr = std::min(crow, rows - r0);
         const size_t off = size_t(r0) * d_out * eb, bytes = size_t(nr) * d_out * eb;
-        cudaEvent_t ein, eout;
-        cudaEventCreateWithFlags(&ein, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&eout, cudaEventDisableTiming);
-        evs.push_back(ein);
-        evs.push_back(eout);
-        cudaMemcpyAsync(static_cast<char*>(dbase) + off, static_cast<const char*>(base) + off,
-                        bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
-        cudaMemcpyAsync(static_cast<char*>(dlora) + off, static_cast<const char*>(lora) + off,
-                        bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
-        cudaEventRecord(ein, ctx->st_h2d);
-        cudaStreamWaitEvent(ctx->st_comp, ein, 0);
+        auto at = [&](void* p) { return static_cast<char*>(p) + off; };
+        auto atc = [&](const void* p) { return static_cast<const char*>(p) + off; };
+        hc.copy(at(dbase), atc(base), bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        hc.copy(at(dlora), atc(lora), bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        if (!hc.link(ctx->st_h2d, ctx->st_comp)) return cuda_fail(hc.first, hc.where);
         int launches = 0;
-        e = dfx::launch_compose_fwd(dtype, static_cast<char*>(dbase) + off,
-                                    static_cast<char*>(dlora) + off, dg, static_cast<float>(s), nr,
-                                    d_out, static_cast<char*>(ddelta) + off, nullptr, ctx->st_comp,
-                                    &launches);
+        e = dfx::launch_compose_fwd(dtype, at(dbase), at(dlora), dg_, static_cast<float>(s), nr,
+                                    d_out, at(ddelta), nullptr, ctx->st_comp, &launches);
         ctx->launches += launches;
         if (e != cudaSuccess) return cuda_fail(e, "dfx_module_fwd_host/compose");
-        cudaEventRecord(eout, ctx->st_comp);
-        cudaStreamWaitEvent(ctx->st_d2h, eout, 0);
-        cudaMemcpyAsync(static_cast<char*>(delta) + off, static_cast<char*>(ddelta) + off, bytes,
-                        cudaMemcpyDeviceToHost, ctx->st_d2h);
+        if (!hc.link(ctx->st_comp, ctx->st_d2h) ||
+            !hc.copy(static_cast<char*>(delta) + off, at(ddelta), bytes, cudaMemcpyDeviceToHost,
+                     ctx->st_d2h))
+            return cuda_fail(hc.first, hc.where);
     }
-    e = cudaStreamSynchronize(ctx->st_d2h);
-    cudaEventDestroy(ev_norm);
-    cudaEventDestroy(ev_w);
-    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+    e = hc.drain();
     if (e == cudaSuccess) e = cudaGetLastError();
-    return finish_call(e, "dfx_module_fwd_host");
+    return finish_call(ctx, e, "dfx_module_fwd_host");
 }
 
 int dfx_module_train_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A,
@@ -756,20 +1028,15 @@ int dfx_module_train_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const vo
                           const void* dy, double s, int64_t d_out, int64_t d_in, int64_t r,
                           int64_t rows, int64_t chunk_size, void* delta, void* d_lora,
                           void* d_base, float* d_mag, float* g) {
-    int rc = enter(ctx);
+    DeviceGuard dg;
+    int rc = enter(ctx, dg);
     if (rc) return rc;
     rc = check_norm_args(dtype, W, A, B, d_out, d_in, r, chunk_size);
     if (rc) return rc;
     if (rows < 0 || !m || !g || !d_mag ||
         (rows > 0 && (!base || !lora || !dy || !delta || !d_lora || !d_base)))
         return fail(DFX_EINVAL, "dfx_module_train_host: null operand");
-    cudaError_t e = cudaSuccess;
-    if (!ctx->st_h2d) {
-        if ((e = cudaStreamCreateWithFlags(&ctx->st_h2d, cudaStreamNonBlocking)) != cudaSuccess ||
-            (e = cudaStreamCreateWithFlags(&ctx->st_comp, cudaStreamNonBlocking)) != cudaSuccess ||
-            (e = cudaStreamCreateWithFlags(&ctx->st_d2h, cudaStreamNonBlocking)) != cudaSuccess)
-            return cuda_fail(e, "stream create");
-    }
+    if ((rc = host_streams(ctx))) return rc;
     const size_t eb = dtype == DFX_F32 ? 4 : 2;
     const size_t nW = size_t(d_out) * d_in, nA = size_t(r) * d_in, nB = size_t(d_out) * r;
     const size_t nact = size_t(rows) * d_out;
@@ -777,39 +1044,31 @@ int dfx_module_train_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const vo
                               size_t(d_out) * 4, nact * eb, nact * eb, nact * eb, nact * eb,
                               nact * eb, nact * eb, nact * eb, size_t(d_out) * 4};
     void* buf[14];
+    cudaError_t e = cudaSuccess;
     for (int i = 0; i < 14; ++i) {
         buf[i] = stage_buf(ctx, i, sizes[i], &e);
         if (e) return cuda_fail(e, "stage alloc");
     }
     void *dW = buf[0], *dA = buf[1], *dB = buf[2];
-    float *dm = static_cast<float*>(buf[3]), *dg = static_cast<float*>(buf[4]);
+    float *dm = static_cast<float*>(buf[3]), *dg_ = static_cast<float*>(buf[4]);
     float* dwn = static_cast<float*>(buf[5]);
     void *dbase = buf[6], *dlora = buf[7], *ddelta = buf[8], *dinner = buf[9], *ddy = buf[10];
     void *ddl = buf[11], *ddb = buf[12];
     float* ddm = static_cast<float*>(buf[13]);
 
-    std::vector<cudaEvent_t> evs;
-    auto event = [&]() {
-        cudaEvent_t ev;
-        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-        evs.push_back(ev);
-        return ev;
-    };
+    HostCall hc(ctx);
     // weights first: the norm overlaps the activation upload
-    cudaMemcpyAsync(dA, A, nA * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
-    cudaMemcpyAsync(dB, B, nB * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
-    cudaMemcpyAsync(dm, m, d_out * 4, cudaMemcpyHostToDevice, ctx->st_h2d);
-    cudaMemcpyAsync(dW, W, nW * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
-    cudaEvent_t ev_w = event();
-    cudaEventRecord(ev_w, ctx->st_h2d);
-    cudaStreamWaitEvent(ctx->st_comp, ev_w, 0);
+    hc.copy(dA, A, nA * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
+    hc.copy(dB, B, nB * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
+    hc.copy(dm, m, d_out * 4, cudaMemcpyHostToDevice, ctx->st_h2d);
+    hc.copy(dW, W, nW * eb, cudaMemcpyHostToDevice, ctx->st_h2d);
+    if (!hc.link(ctx->st_h2d, ctx->st_comp)) return cuda_fail(hc.first, hc.where);
     rc = run_norm(ctx, dtype, dW, dA, dB, d_out, d_in, r, s, chunk_size, nullptr, nullptr,
-                  nullptr, dm, dtype, dwn, dg, dtype, ctx->st_comp, "dfx_module_train_host/norm");
+                  nullptr, dm, dtype, dwn, dg_, dtype, ctx->st_comp, "dfx_module_train_host/norm");
     if (rc) return rc;
-    cudaEvent_t ev_norm = event();
-    cudaEventRecord(ev_norm, ctx->st_comp);
-    cudaStreamWaitEvent(ctx->st_d2h, ev_norm, 0);
-    cudaMemcpyAsync(g, dg, d_out * 4, cudaMemcpyDeviceToHost, ctx->st_d2h);
+    if (!hc.link(ctx->st_comp, ctx->st_d2h) ||
+        !hc.copy(g, dg_, d_out * 4, cudaMemcpyDeviceToHost, ctx->st_d2h))
+        return cuda_fail(hc.first, hc.where);
 
     // Row chunks: upload base / lora / dY of chunk c+1 while chunk c runs the dual compose and
     // the elementwise backward (d_lora, d_base) and chunk c-1 downloads delta / d_lora /
@@ -822,44 +1081,39 @@ int dfx_module_train_host(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const vo
         const size_t off = size_t(r0) * d_out * eb, bytes = size_t(nr) * d_out * eb;
         auto at = [&](void* p) { return static_cast<char*>(p) + off; };
         auto atc = [&](const void* p) { return static_cast<const char*>(p) + off; };
-        cudaMemcpyAsync(at(dbase), atc(base), bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
-        cudaMemcpyAsync(at(dlora), atc(lora), bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
-        cudaMemcpyAsync(at(ddy), atc(dy), bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
-        cudaEvent_t ein = event();
-        cudaEventRecord(ein, ctx->st_h2d);
-        cudaStreamWaitEvent(ctx->st_comp, ein, 0);
+        hc.copy(at(dbase), atc(base), bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        hc.copy(at(dlora), atc(lora), bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        hc.copy(at(ddy), atc(dy), bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        if (!hc.link(ctx->st_h2d, ctx->st_comp)) return cuda_fail(hc.first, hc.where);
         int launches = 0;
-        e = dfx::launch_compose_fwd(dtype, at(dbase), at(dlora), dg, static_cast<float>(s), nr,
+        e = dfx::launch_compose_fwd(dtype, at(dbase), at(dlora), dg_, static_cast<float>(s), nr,
                                     d_out, at(ddelta), at(dinner), ctx->st_comp, &launches);
         if (e == cudaSuccess)
-            e = dfx::launch_compose_bwd(dtype, at(ddy), dg, static_cast<float>(s), nullptr, nullptr,
-                                        nr, d_out, at(ddl), at(ddb), nullptr, ctx->st_comp,
-                                        &launches);
+            e = dfx::launch_compose_bwd(dtype, at(ddy), dg_, static_cast<float>(s), nullptr,
+                                        nullptr, nr, d_out, at(ddl), at(ddb), nullptr,
+                                        ctx->st_comp, &launches);
         ctx->launches += launches;
         if (e != cudaSuccess) return cuda_fail(e, "dfx_module_train_host/compose");
-        cudaEvent_t eout = event();
-        cudaEventRecord(eout, ctx->st_comp);
-        cudaStreamWaitEvent(ctx->st_d2h, eout, 0);
-        cudaMemcpyAsync(static_cast<char*>(delta) + off, at(ddelta), bytes, cudaMemcpyDeviceToHost,
-                        ctx->st_d2h);
-        cudaMemcpyAsync(static_cast<char*>(d_lora) + off, at(ddl), bytes, cudaMemcpyDeviceToHost,
-                        ctx->st_d2h);
-        cudaMemcpyAsync(static_cast<char*>(d_base) + off, at(ddb), bytes, cudaMemcpyDeviceToHost,
-                        ctx->st_d2h);
+        if (!hc.link(ctx->st_comp, ctx->st_d2h) ||
+            !hc.copy(static_cast<char*>(delta) + off, at(ddelta), bytes, cudaMemcpyDeviceToHost,
+                     ctx->st_d2h) ||
+            !hc.copy(static_cast<char*>(d_lora) + off, at(ddl), bytes, cudaMemcpyDeviceToHost,
+                     ctx->st_d2h) ||
+            !hc.copy(static_cast<char*>(d_base) + off, at(ddb), bytes, cudaMemcpyDeviceToHost,
+                     ctx->st_d2h))
+            return cuda_fail(hc.first, hc.where);
     }
     int launches = 0;
-    e = dfx::launch_compose_bwd(dtype, ddy, dg, static_cast<float>(s), dinner, dwn, rows, d_out,
+    e = dfx::launch_compose_bwd(dtype, ddy, dg_, static_cast<float>(s), dinner, dwn, rows, d_out,
                                 nullptr, nullptr, ddm, ctx->st_comp, &launches);
     ctx->launches += launches;
     if (e != cudaSuccess) return cuda_fail(e, "dfx_module_train_host/d_mag");
-    cudaEvent_t ev_bwd = event();
-    cudaEventRecord(ev_bwd, ctx->st_comp);
-    cudaStreamWaitEvent(ctx->st_d2h, ev_bwd, 0);
-    cudaMemcpyAsync(d_mag, ddm, d_out * 4, cudaMemcpyDeviceToHost, ctx->st_d2h);
-    e = cudaStreamSynchronize(ctx->st_d2h);
-    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+    if (!hc.link(ctx->st_comp, ctx->st_d2h) ||
+        !hc.copy(d_mag, ddm, d_out * 4, cudaMemcpyDeviceToHost, ctx->st_d2h))
+        return cuda_fail(hc.first, hc.where);
+    e = hc.drain();
     if (e == cudaSuccess) e = cudaGetLastError();
-    return finish_call(e, "dfx_module_train_host");
+    return finish_call(ctx, e, "dfx_module_train_host");
 }
 
 }  // extern "C"

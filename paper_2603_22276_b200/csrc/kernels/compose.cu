@@ -470,9 +470,7 @@ cudaError_t fwd_impl(const void* base, const void* lora, const float* g, float s
         const int64_t gy = std::min<int64_t>((rows + by * R - 1) / (by * R), 65535);
         // prefetch distance: one wave of resident CTAs (2 per SM at this register count);
         // measured at C2: dual 45.8 -> 43.3 us, 71 -> 61 us on a 76-SM partition
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int sms = device_sm_count();
         const int pf_rows = static_cast<int>(2 * sms / gx) * by * R;
         prof_begin(kInner ? "compose_fwd_dual" : "compose_fwd", st);
         compose_fwd_vec<T, kInner, R>
@@ -548,9 +546,7 @@ cudaError_t bwd_impl(int dt, const void* dy, const float* g, float sf, const voi
         // one CTA per 128-byte column slab runs the whole column height; when the slabs
         // outnumber two per SM, a shallower ring (3 stages, ~49 KB) lets four share an SM so
         // the grid stays one wave (C3: 448 slabs)
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int sms = device_sm_count();
         const int64_t slabs = (d_out + SerialCfg<T>::kSC - 1) / SerialCfg<T>::kSC;
         // beside the norm GEMMs (an SM budget is set): 256-byte slabs, half as many CTAs, each
         // filling an SM — measured +1.5-2.7 % on the pipelined C2 training step (A/B on one

@@ -23,6 +23,11 @@ cudaError_t make_tmap_2d_sw(CUtensorMap* out, int dt, const void* base, uint64_t
                             uint64_t cols, uint64_t row_pitch_bytes, uint32_t box_cols,
                             uint32_t box_rows, int swizzle_bytes);
 
+// Attributes of the current device, queried once per device and cached (launch paths call
+// these on every launch).
+int device_sm_count();
+int device_smem_optin();
+
 // cudaFuncAttributeMaxDynamicSharedMemorySize for `func` on the current device, set once per
 // (function, device) pair (thread-safe; a process may drive several devices).
 cudaError_t ensure_max_dyn_smem(const void* func, int bytes);
@@ -92,6 +97,20 @@ enum NormMode : int { kNormFull = 0, kNormPartial = 1, kNormFinish = 2 };
 // profiling context.
 void prof_begin(const char* name, cudaStream_t st);
 void prof_end(cudaStream_t st);
+
+// ------------------------------------------------------------ symmetric all-reduce (comm.cu)
+constexpr int kCommMaxRanks = 16;
+constexpr int kCommMaxBlocks = 64;
+constexpr int kCommThreads = 512;
+struct CommArgs {
+    char* peers[kCommMaxRanks];   // every rank's symmetric allocation, mapped here (rank order)
+    int rank, world;
+    int64_t count;                // fp32 elements reduced
+    float* out;                   // local result [count]
+    size_t start_off, end_off, epoch_off, err_off;   // byte offsets inside an allocation
+    int max_blocks;               // identical on every rank (block b pairs with block b)
+};
+cudaError_t launch_allreduce(const CommArgs& a, cudaStream_t st, int* launches);
 
 struct Workspace;  // owned by the context (dfx_capi.cu)
 void* ws_get(Workspace* ws, int slot, size_t bytes, cudaError_t* err);

@@ -370,10 +370,7 @@ cudaError_t launch_lora_compose(int dt, const void* mid, const void* b, const vo
     p.kb = static_cast<int>((r + kLK - 1) / kLK);
     p.m_tiles = static_cast<int>((rows + kLM - 1) / kLM);
     p.tiles = static_cast<int>(p.m_tiles * ((d_out + kLN - 1) / kLN));
-    int dev = 0, sms = 148, optin = 227 * 1024;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int sms = device_sm_count(), optin = device_smem_optin();
     auto kern = dt == kBF16 ? lora_compose_kernel<__nv_bfloat16> : lora_compose_kernel<__half>;
     cudaFuncAttributes fa{};
     e = cudaFuncGetAttributes(&fa, kern);

@@ -19,7 +19,8 @@ enum WsSlot : int {
     kWsGram = 5,       // G fp32               [r][r]          (SIMT path)
     kWsTerms = 6,      // base_sq/cross/ba_sq  [3][d_out]      (when caller wants none)
     kWsGramCount = 7,  // per-tile split counters for the fused Gram reduction (zeroed)
-    kWsCount = 8
+    kWsScale = 8,      // fp16 V operand: 2^-e of the scaled Gram split (one float)
+    kWsCount = 9
 };
 
 struct FinishArgs {

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "norm_common.cuh"
 
@@ -60,6 +61,7 @@ struct TcParams {
     int tiles;              // tiles per K split (the persistent loop's extent)
     int w_prefetch;         // K blocks of X (W) prefetched into L2 ahead of the loads
     int nh;                 // pair kernel: UMMAs per K step (N per CTA pair = nh * bn)
+    const float* out_scale; // rowdot: multiply each row's sum by *out_scale (fp16 V: 2^-e)
 };
 
 __device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
@@ -70,6 +72,25 @@ __device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
         f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
     }
 }
+
+// Eight 16-bit elements of the operand dtype (kEl = kBF16 or kF16) widened to fp32 (exact).
+template <int kEl>
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+    if (kEl == kBF16) {
+        unpack_bf16x8(v, f);
+    } else {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 t = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+            f[2 * i] = t.x;
+            f[2 * i + 1] = t.y;
+        }
+    }
+}
+
+// kind::f16 instruction-descriptor operand format: 1 = bf16, 0 = fp16.
+__host__ __device__ constexpr uint32_t ab_fmt(int el) { return el == kBF16 ? 1u : 0u; }
 
 // The base_sq chain of a row tile (4 units of 32 rows) is spread over the CTAs that
 // share the tile (its N splits): unit u belongs to the CTA whose N index is u*n_split/4.
@@ -101,11 +122,12 @@ __device__ __forceinline__ int chain_active_warps(int n_idx, int n_split) {
 // ChainPlan chunk (factored_norm.cpp:52-60); partials go to base_out[chunk][row] and the
 // finisher adds them in ascending order (:60), so base_sq is bitwise the reference's.
 // The stage is released only after the chain consumed its registers.
-template <int kRows, bool kF32 = false>
+template <int kRows, int kEl = kBF16>
 __device__ __forceinline__ void chain_tile(const ChainUnits& cu, const uint8_t* smem,
                                            int stage_bytes, uint64_t* ready, uint64_t* empty,
                                            int stages, int start, int nkb, int kb0, int64_t chunk,
                                            int64_t m0, int64_t M, float* base_out, int lane) {
+    constexpr bool kIsF32 = kEl == kF32;
     int s = start % stages;
     uint32_t ph = static_cast<uint32_t>((start / stages) & 1);
     float part[kRows];
@@ -115,7 +137,7 @@ __device__ __forceinline__ void chain_tile(const ChainUnits& cu, const uint8_t* 
         part[j] = 0.0f;
         row[j] = 32 * cu.u[j] + lane;
     }
-    int64_t kpos = int64_t(kb0) * (kF32 ? 32 : 64);
+    int64_t kpos = int64_t(kb0) * (kIsF32 ? 32 : 64);
     int64_t cur = kpos / chunk;
     int64_t boundary = (cur + 1) * chunk;
     for (int it = 0; it < nkb; ++it) {
@@ -139,15 +161,15 @@ __device__ __forceinline__ void chain_tile(const ChainUnits& cu, const uint8_t* 
         }
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-            constexpr int kE = kF32 ? 4 : 8;               // elements per 16-byte chunk
+            constexpr int kE = kIsF32 ? 4 : 8;             // elements per 16-byte chunk
             float f[kRows][8];
 #pragma unroll
             for (int j = 0; j < kRows; ++j) {
-                if (kF32) {
+                if (kIsF32) {
                     f[j][0] = __uint_as_float(v[j][c].x); f[j][1] = __uint_as_float(v[j][c].y);
                     f[j][2] = __uint_as_float(v[j][c].z); f[j][3] = __uint_as_float(v[j][c].w);
                 } else {
-                    unpack_bf16x8(v[j][c], f[j]);
+                    unpack8<kEl>(v[j][c], f[j]);
                 }
             }
 #pragma unroll
@@ -158,7 +180,7 @@ __device__ __forceinline__ void chain_tile(const ChainUnits& cu, const uint8_t* 
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        kpos += kF32 ? 32 : 64;
+        kpos += kIsF32 ? 32 : 64;
         if (++s == stages) { s = 0; ph ^= 1; }
     }
 #pragma unroll
@@ -191,27 +213,28 @@ __device__ __forceinline__ void tile_coords(int kMode, const TcParams& p, int t,
 // fp32-class accumulation on the tensor cores.
 constexpr int kSplitWarps = 4;                   // 3xTF32: warps 6 .. 6 + kSplitWarps - 1
 
-template <int kMode, bool kF32 = false>
-__global__ void __launch_bounds__(kF32 ? kThreads + 32 * (kSplitWarps - 2) : kThreads, 1)
+template <int kMode, int kEl = kBF16>
+__global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2) : kThreads, 1)
     tc_rowdot(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
               const TcParams p) {
+    constexpr bool kIsF32 = kEl == dfx::kF32;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     const int y_stage = p.bn * kBK * 2;
     const int raw_bytes = kXStage + y_stage;    // both multiples of 1024
-    const int stage_bytes = kF32 ? 2 * raw_bytes : raw_bytes;   // [raw X | raw Y | lo X | lo Y]
+    const int stage_bytes = kIsF32 ? 2 * raw_bytes : raw_bytes;   // [raw X | raw Y | lo X | lo Y]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
     uint64_t* empty = full + p.stages;
     uint64_t* tmem_full = empty + p.stages;     // [2]
     uint64_t* tmem_empty = tmem_full + 2;       // [2]
-    uint64_t* split = tmem_empty + 2;           // [stages] (kF32: low parts written)
+    uint64_t* split = tmem_empty + 2;           // [stages] (kIsF32: low parts written)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(split + p.stages);
 
     const int warp = warp_id(), lane = lane_id();
     const int ks = blockIdx.y;
     const int kb0 = ks * p.kb_per_split;
-    constexpr int kBKe = kF32 ? 32 : kBK;       // K elements per 128-byte block
+    constexpr int kBKe = kIsF32 ? 32 : kBK;       // K elements per 128-byte block
     const int64_t total_kb = (p.k_total + kBKe - 1) / kBKe;
     const int64_t kb_left = total_kb - kb0;
     const int nkb = static_cast<int>(kb_left < p.kb_per_split ? kb_left : p.kb_per_split);
@@ -272,7 +295,7 @@ __global__ void __launch_bounds__(kF32 ? kThreads + 32 * (kSplitWarps - 2) : kTh
                     mbar_arrive_expect_tx(&full[s], raw_bytes);
                     uint8_t* sx = smem + s * stage_bytes;
                     uint8_t* sy = sx + kXStage;
-                    const int kc = (kb0 + it) * (kF32 ? 32 : kBK);
+                    const int kc = (kb0 + it) * (kIsF32 ? 32 : kBK);
                     const int kx = (p.x_kwrap && kc >= p.x_kwrap) ? kc - p.x_kwrap : kc;
                     tma_load_2d(&tmx, &full[s], sx, kx, static_cast<int32_t>(m0), pol_x);
                     tma_load_2d(&tmy, &full[s], sy, kc, static_cast<int32_t>(n0), pol_y);
@@ -283,8 +306,8 @@ __global__ void __launch_bounds__(kF32 ? kThreads + 32 * (kSplitWarps - 2) : kTh
     } else if (nkb > 0 && warp == kWarpMma) {
         // ================= MMA issuer (single thread) =================
         if (lane == 0) {
-            const uint32_t idesc = kF32 ? umma_idesc_tf32(kBM, static_cast<uint32_t>(p.bn))
-                                        : umma_idesc_f16(1u, kBM, static_cast<uint32_t>(p.bn));
+            const uint32_t idesc = kIsF32 ? umma_idesc_tf32(kBM, static_cast<uint32_t>(p.bn))
+                                        : umma_idesc_f16(ab_fmt(kEl), kBM, static_cast<uint32_t>(p.bn));
             int s = 0;
             uint32_t ph = 0;
             int local = 0;
@@ -297,7 +320,7 @@ __global__ void __launch_bounds__(kF32 ? kThreads + 32 * (kSplitWarps - 2) : kTh
                 mbar_wait(&tmem_empty[slot], ((local >> 1) & 1) ^ 1);
                 tc_fence_after();
                 for (int it = 0; it < nkb; ++it) {
-                    mbar_wait(kF32 ? &split[s] : &full[s], ph);
+                    mbar_wait(kIsF32 ? &split[s] : &full[s], ph);
                     tc_fence_after();
                     const uint32_t sx = smem_u32(smem + s * stage_bytes);
                     const uint32_t sy = sx + kXStage;
@@ -305,7 +328,7 @@ __global__ void __launch_bounds__(kF32 ? kThreads + 32 * (kSplitWarps - 2) : kTh
                     for (int k = 0; k < 4; ++k) {
                         const uint64_t ad = umma_desc_k_sw128(sx + k * 32);
                         const uint64_t bd = umma_desc_k_sw128(sy + k * 32);
-                        if (kF32) {
+                        if (kIsF32) {
                             const uint64_t adl = umma_desc_k_sw128(sx + raw_bytes + k * 32);
                             const uint64_t bdl = umma_desc_k_sw128(sy + raw_bytes + k * 32);
                             umma_tf32(tacc, ad, bd, idesc, (it > 0 || k > 0) ? 1u : 0u);
@@ -323,7 +346,7 @@ __global__ void __launch_bounds__(kF32 ? kThreads + 32 * (kSplitWarps - 2) : kTh
                 umma_commit(&tmem_full[slot]);
             }
         }
-    } else if (kF32 && nkb > 0 && warp >= 6) {
+    } else if (kIsF32 && nkb > 0 && warp >= 6) {
         // ================= 3xTF32 split: low parts x - tf32(x) of both tiles ==========
         const int st = (warp - 6) * 32 + lane;                  // 0 .. 32 * kSplitWarps - 1
         constexpr int kST = 32 * kSplitWarps;
@@ -378,10 +401,10 @@ __global__ void __launch_bounds__(kF32 ? kThreads + 32 * (kSplitWarps - 2) : kTh
             if (do_chain) {
                 const ChainUnits cu = chain_units(warp, static_cast<int>(t % p.n_split), p.n_split);
                 if (cu.n == 2)
-                    chain_tile<2, kF32>(cu, smem, stage_bytes, full, empty, p.stages, local * nkb, nkb,
+                    chain_tile<2, kEl>(cu, smem, stage_bytes, full, empty, p.stages, local * nkb, nkb,
                                         kb0, p.chunk, m0, p.M, p.base_out, lane);
                 else if (cu.n == 1)
-                    chain_tile<1, kF32>(cu, smem, stage_bytes, full, empty, p.stages, local * nkb, nkb,
+                    chain_tile<1, kEl>(cu, smem, stage_bytes, full, empty, p.stages, local * nkb, nkb,
                                         kb0, p.chunk, m0, p.M, p.base_out, lane);
             }
             // ---- epilogue: TMEM accumulator -> rowdot / tile store
@@ -402,16 +425,16 @@ __global__ void __launch_bounds__(kF32 ? kThreads + 32 * (kSplitWarps - 2) : kTh
                             // columns past the tile (bn % 32 != 0) belong to the other slot
                             if (c0 + 8 * v < p.bn && n0 + c0 + 8 * v < p.N) {
                                 float z[8];
-                                if (kF32) {
+                                if (kIsF32) {
                                     const float* zr = static_cast<const float*>(p.Z) + gm * p.ldz + n0 + c0;
                                     const float4 z0 = *reinterpret_cast<const float4*>(zr + 8 * v);
                                     const float4 z1 = *reinterpret_cast<const float4*>(zr + 8 * v + 4);
                                     z[0] = z0.x; z[1] = z0.y; z[2] = z0.z; z[3] = z0.w;
                                     z[4] = z1.x; z[5] = z1.y; z[6] = z1.z; z[7] = z1.w;
                                 } else {
-                                    const __nv_bfloat16* zr =
-                                        static_cast<const __nv_bfloat16*>(p.Z) + gm * p.ldz + n0 + c0;
-                                    unpack_bf16x8(*reinterpret_cast<const uint4*>(zr + 8 * v), z);
+                                    const uint16_t* zr =
+                                        static_cast<const uint16_t*>(p.Z) + gm * p.ldz + n0 + c0;
+                                    unpack8<kEl>(*reinterpret_cast<const uint4*>(zr + 8 * v), z);
                                 }
 #pragma unroll
                                 for (int e = 0; e < 8; ++e)
@@ -423,6 +446,7 @@ __global__ void __launch_bounds__(kF32 ? kThreads + 32 * (kSplitWarps - 2) : kTh
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tmem_empty[slot]);
+                if (p.out_scale) acc = __fmul_rn(acc, *p.out_scale);   // exact power of two
                 if (gm < p.M) p.out[(int64_t(ks) * p.n_split + (n0 / p.bn)) * p.M + gm] = acc;
             } else {
                 // gram tile store: out[(ks * tiles + t) * 128*bn + row*bn + col]
@@ -469,6 +493,7 @@ __global__ void __launch_bounds__(kF32 ? kThreads + 32 * (kSplitWarps - 2) : kTh
 // (whose chain warps read their own W rows) and multicasts its commits to both CTAs'
 // empty / tmem_full barriers; both CTAs' epilogue warps release the accumulator slot on
 // the leader's tmem_empty barrier.
+template <int kEl>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_pair_rowdot(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
                    const TcParams p) {
@@ -567,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (nkb > 0 && warp == kWarpMma) {
         // ================= MMA issuer (leader CTA, single thread) =================
         if (leader && lane == 0) {
-            const uint32_t idesc = umma_idesc_f16(1u, 2 * kBM, static_cast<uint32_t>(p.bn));
+            const uint32_t idesc = umma_idesc_f16(ab_fmt(kEl), 2 * kBM, static_cast<uint32_t>(p.bn));
             int s = 0;
             uint32_t ph = 0;
             int local = 0;
@@ -640,10 +665,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (do_chain) {
                 const ChainUnits cu = chain_units(warp, static_cast<int>(t % p.n_split), p.n_split);
                 if (cu.n == 2)
-                    chain_tile<2>(cu, smem, stage_bytes, ready, empty, p.stages, local * nkb, nkb, kb0,
+                    chain_tile<2, kEl>(cu, smem, stage_bytes, ready, empty, p.stages, local * nkb, nkb, kb0,
                                   p.chunk, m0, p.M, p.base_out, lane);
                 else if (cu.n == 1)
-                    chain_tile<1>(cu, smem, stage_bytes, ready, empty, p.stages, local * nkb, nkb, kb0,
+                    chain_tile<1, kEl>(cu, smem, stage_bytes, ready, empty, p.stages, local * nkb, nkb, kb0,
                                   p.chunk, m0, p.M, p.base_out, lane);
             }
             const int slot = nslots == 2 ? (local & 1) : 0;
@@ -661,12 +686,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld_32x32b_x32(trow + c0, u);
                 tmem_ld_wait();
                 if (gm < p.M) {
-                    const __nv_bfloat16* zr = static_cast<const __nv_bfloat16*>(p.Z) + gm * p.ldz + n0 + c0;
+                    const uint16_t* zr = static_cast<const uint16_t*>(p.Z) + gm * p.ldz + n0 + c0;
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
                         if (c0 + 8 * v < bn_pair && n0 + c0 + 8 * v < p.N) {
                             float z[8];
-                            unpack_bf16x8(*reinterpret_cast<const uint4*>(zr + 8 * v), z);
+                            unpack8<kEl>(*reinterpret_cast<const uint4*>(zr + 8 * v), z);
 #pragma unroll
                             for (int e = 0; e < 8; ++e)
                                 acc = fmaf(__uint_as_float(u[8 * v + e]), z[e], acc);
@@ -727,16 +752,46 @@ __global__ void __launch_bounds__(256) gram_reduce(const float* __restrict__ par
     g2[i * 2 * r_pad + r_pad + j] = lo;
 }
 
-// d_in-split finish: the all-reduced fp32 Gram -> [G_hi | G_lo] (bf16, K padded with 0).
+// fp32 Gram -> [G_hi | G_lo] (K padded with 0) as the V GEMM's operand.
+// bf16: hi = bf16(G), lo = bf16(G - hi), unscaled (bf16 has fp32's range).
+// fp16: fp16's range (|x| <= 65504, normal >= 2^-14) cannot hold a Gram of arbitrary scale,
+//   so G is scaled by 2^e first, e = 14 - ilogb(max diag G) (|G_lq| <= max diag, G is PSD), so
+//   the largest entry lands in [2^14, 2^15); the V epilogue multiplies each row's sum by 2^-e
+//   (exact).  Every block finds the max diagonal itself (r <= 2048 reads), so no extra pass.
+//   Non-finite diagonals (NaN / inf in A) leave e = 0 and propagate.
+template <typename T>
 __global__ void __launch_bounds__(256) gram_split(const float* __restrict__ g, int64_t r,
-                                                  int64_t r_pad, __nv_bfloat16* __restrict__ g2) {
+                                                  int64_t r_pad, T* __restrict__ g2,
+                                                  float* __restrict__ inv_scale) {
+    constexpr bool kHalf = std::is_same<T, __half>::value;
+    float scale = 1.0f;
+    if (kHalf) {
+        __shared__ float red[8];
+        float mx = 0.0f;
+        bool bad = false;
+        for (int64_t i = threadIdx.x; i < r; i += blockDim.x) {
+            const float d = g[i * r + i];
+            bad |= !isfinite(d);
+            mx = fmaxf(mx, fabsf(d));
+        }
+        bad = __syncthreads_or(bad);
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+        __syncthreads();
+        mx = red[0];
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) mx = fmaxf(mx, red[w]);
+        int e = 0;
+        if (!bad && mx > 0.0f) e = max(-120, min(120, 14 - ilogbf(mx)));
+        scale = ldexpf(1.0f, e);
+        if (blockIdx.x == 0 && threadIdx.x == 0) *inv_scale = ldexpf(1.0f, -e);
+    }
     const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= r * r_pad) return;
     const int64_t i = idx / r_pad, j = idx % r_pad;
-    const float v = j < r ? g[i * r + j] : 0.0f;
-    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    const float v = j < r ? __fmul_rn(g[i * r + j], scale) : 0.0f;
+    const T hi = Elem<T>::from_f(v);
     g2[i * 2 * r_pad + j] = hi;
-    g2[i * 2 * r_pad + r_pad + j] = __float2bfloat16_rn(__fsub_rn(v, __bfloat162float(hi)));
+    g2[i * 2 * r_pad + r_pad + j] = Elem<T>::from_f(__fsub_rn(v, Elem<T>::to_f(hi)));
 }
 
 int stages_for(int bn, bool f32 = false) {
@@ -754,11 +809,13 @@ size_t smem_for(int bn, int stages, bool f32 = false) {
 // a whole TPC; a lone side CTA per TPC would strand its sibling SM).
 cudaError_t launch_tc(int mode, const CUtensorMap& tx, const CUtensorMap& ty, TcParams p,
                       dim3 grid, cudaStream_t st, const char* name, bool tpc_pairs = false,
-                      bool f32 = false) {
+                      int el = kBF16) {
+    const bool f32 = el == kF32;
     const size_t smem = smem_for(p.bn, p.stages, f32);
     cudaError_t e;
-    auto kern = f32 ? (mode == kTcRowdot ? tc_rowdot<kTcRowdot, true> : tc_rowdot<kTcStore, true>)
-                    : (mode == kTcRowdot ? tc_rowdot<kTcRowdot> : tc_rowdot<kTcStore>);
+    auto kern = el == kF32   ? (mode == kTcRowdot ? tc_rowdot<kTcRowdot, kF32> : tc_rowdot<kTcStore, kF32>)
+                : el == kF16 ? (mode == kTcRowdot ? tc_rowdot<kTcRowdot, kF16> : tc_rowdot<kTcStore, kF16>)
+                             : (mode == kTcRowdot ? tc_rowdot<kTcRowdot, kBF16> : tc_rowdot<kTcStore, kBF16>);
     if ((e = ensure_max_dyn_smem(reinterpret_cast<const void*>(kern), kMaxSmem)) != cudaSuccess) return e;
     if (tpc_pairs) grid.x = (grid.x + 1) / 2 * 2;
     cudaLaunchConfig_t cfg = {};
@@ -790,9 +847,10 @@ int stages_for_pair(int bn, int nh = 1) {
 }
 
 cudaError_t launch_tc_pair(const CUtensorMap& tx, const CUtensorMap& ty, TcParams p, int pairs,
-                           int ks, cudaStream_t st, const char* name) {
+                           int ks, cudaStream_t st, const char* name, int el) {
     cudaError_t e;
-    if ((e = ensure_max_dyn_smem(reinterpret_cast<const void*>(tc_pair_rowdot), kMaxSmem)) != cudaSuccess)
+    auto kern = el == kF16 ? tc_pair_rowdot<kF16> : tc_pair_rowdot<kBF16>;
+    if ((e = ensure_max_dyn_smem(reinterpret_cast<const void*>(kern), kMaxSmem)) != cudaSuccess)
         return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs, ks, 1);
@@ -807,7 +865,7 @@ cudaError_t launch_tc_pair(const CUtensorMap& tx, const CUtensorMap& ty, TcParam
     cfg.attrs = at;
     cfg.numAttrs = 1;
     prof_begin(name, st);
-    e = cudaLaunchKernelEx(&cfg, tc_pair_rowdot, tx, ty, p);
+    e = cudaLaunchKernelEx(&cfg, kern, tx, ty, p);
     prof_end(st);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -861,7 +919,7 @@ bool pair_enabled() {
 }
 
 bool norm_tc_supported(int dt, int64_t d_out, int64_t d_in, int64_t r) {
-    return dt == kBF16 && d_in >= 64 && d_in % 8 == 0 && r % 8 == 0 && r >= 16 && r <= 2048 &&
+    return (dt == kBF16 || dt == kF16) && d_in >= 64 && d_in % 8 == 0 && r % 8 == 0 && r >= 16 && r <= 2048 &&
            d_out >= 1 && d_in < (int64_t(1) << 31) && d_out < (int64_t(1) << 31);
 }
 
@@ -1073,6 +1131,17 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
     float* ba = static_cast<float*>(
         ws_get(ws, kWsBa, size_t(plan.sb.ns) * d_out * sizeof(float), &err));
     if (err != cudaSuccess) return err;
+    // fp16 operands: the Gram goes through fp32 and a scaled fp16 hi/lo split (gram_split)
+    const int el = a.dt;
+    const bool half = el == kF16;
+    float* gf32 = nullptr;
+    float* inv_scale = nullptr;
+    if (half && !partial) {
+        gf32 = static_cast<float*>(ws_get(ws, kWsGram, size_t(r) * r * sizeof(float), &err));
+        if (err != cudaSuccess) return err;
+        inv_scale = static_cast<float*>(ws_get(ws, kWsScale, 256, &err));
+        if (err != cudaSuccess) return err;
+    }
 
     cudaStream_t side = st;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -1088,13 +1157,13 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
 
     auto launch_u = [&]() -> cudaError_t {
         CUtensorMap tw, ta;
-        cudaError_t e = make_tmap_2d(&tw, kBF16, a.w, d_out, d_in, d_in * 2, kBK, kBM, true);
+        cudaError_t e = make_tmap_2d(&tw, el, a.w, d_out, d_in, d_in * 2, kBK, kBM, true);
         if (e != cudaSuccess) return e;
         TcParams p{};
         p.M = d_out; p.N = r; p.k_total = d_in; p.kb_per_split = u.kbps;
         p.n_split = u.sp.ns; p.bn = u.sp.bn;
         p.x_kwrap = 0; p.chunk = a.chunk_size;
-        p.Z = static_cast<const __nv_bfloat16*>(a.b); p.ldz = r;
+        p.Z = a.b; p.ldz = r;
         p.out = cross; p.base_out = base; p.do_chain = 1;
         if (a.base_cached) p.do_chain = 0;     // frozen W: base_sq comes from the cache
 #ifdef DFX_KO_CHAIN
@@ -1102,7 +1171,7 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
 #endif
         if (u.pair) {
             // A box = half of the pair's BN rows (each CTA of the pair loads its half)
-            e = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, u.sp.bn / 2, true);
+            e = make_tmap_2d(&ta, el, a.a, r, d_in, d_in * 2, kBK, u.sp.bn / 2, true);
             if (e != cudaSuccess) return e;
             p.nh = u.nh;
             p.stages = stages_for_pair(u.sp.bn, u.nh);
@@ -1112,53 +1181,61 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
                 std::fprintf(stderr, "u plan: pairs %d ks %d kbps %d tiles %d n_split %d bn %d nh %d stages %d"
                              " strategy %d side %d sms %d\n", pairs, u.ks, u.kbps, p.tiles, p.n_split, p.bn,
                              p.nh, p.stages, int(plan.strategy), plan.side, sms);
-            e = launch_tc_pair(tw, ta, p, pairs, u.ks, st, "u_rowdot_tc");
+            e = launch_tc_pair(tw, ta, p, pairs, u.ks, st, "u_rowdot_tc", el);
         } else {
-            e = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, u.sp.bn, true);
+            e = make_tmap_2d(&ta, el, a.a, r, d_in, d_in * 2, kBK, u.sp.bn, true);
             if (e != cudaSuccess) return e;
             p.stages = stages_for(u.sp.bn);
             p.tiles = static_cast<int>(m_tiles * u.sp.ns);
             const int gx = std::min<int>(p.tiles, std::max(1, u.ctas / u.ks));
-            e = launch_tc(kTcRowdot, tw, ta, p, dim3(gx, u.ks), st, "u_rowdot_tc");
+            e = launch_tc(kTcRowdot, tw, ta, p, dim3(gx, u.ks), st, "u_rowdot_tc", false, el);
         }
         if (e == cudaSuccess && launches) ++*launches;
         return e;
     };
     auto launch_gram = [&](cudaStream_t gs) -> cudaError_t {
         CUtensorMap ta;
-        cudaError_t e = make_tmap_2d(&ta, kBF16, a.a, r, d_in, d_in * 2, kBK, kBM, true);
+        cudaError_t e = make_tmap_2d(&ta, el, a.a, r, d_in, d_in * 2, kBK, kBM, true);
         if (e != cudaSuccess) return e;
         TcParams p{};
         p.M = r; p.N = r; p.k_total = d_in; p.kb_per_split = plan.g_kbps; p.n_split = 1;
         p.bn = kBM; p.stages = stages_for(kBM); p.chunk = a.chunk_size;
         p.out = gpart; p.gram_nt = nt; p.tiles = gtiles;
         const int gx = std::min(gtiles, std::max(1, plan.g_ctas / plan.g_ks));
-        e = launch_tc(kTcStore, ta, ta, p, dim3(gx, plan.g_ks), gs, "gram_tc", tpc && gs != st);
+        e = launch_tc(kTcStore, ta, ta, p, dim3(gx, plan.g_ks), gs, "gram_tc", tpc && gs != st, el);
         if (e != cudaSuccess) return e;
         const int64_t n = r * r_pad;
         prof_begin("gram_reduce", gs);
         gram_reduce<<<static_cast<unsigned>((n + 255) / 256), 256, 0, gs>>>(
-            gpart, plan.g_ks, nt, r, r_pad, partial ? nullptr : g2, partial ? a.gram_out : nullptr);
+            gpart, plan.g_ks, nt, r, r_pad, (partial || half) ? nullptr : g2,
+            partial ? a.gram_out : gf32);
         prof_end(gs);
         if (launches) *launches += 2;
+        if ((e = cudaGetLastError()) != cudaSuccess || !half || partial) return e;
+        prof_begin("gram_split", gs);
+        gram_split<__half><<<static_cast<unsigned>((n + 255) / 256), 256, 0, gs>>>(
+            gf32, r, r_pad, reinterpret_cast<__half*>(g2), inv_scale);
+        prof_end(gs);
+        if (launches) *launches += 1;
         return cudaGetLastError();
     };
     auto launch_v = [&](cudaStream_t vs) -> cudaError_t {
         CUtensorMap tb, tg;
-        cudaError_t e = make_tmap_2d(&tb, kBF16, a.b, d_out, r, r * 2, kBK, kBM, true);
+        cudaError_t e = make_tmap_2d(&tb, el, a.b, d_out, r, r * 2, kBK, kBM, true);
         if (e != cudaSuccess) return e;
-        e = make_tmap_2d(&tg, kBF16, g2, r, 2 * r_pad, 2 * r_pad * 2, kBK, plan.sb.bn, true);
+        e = make_tmap_2d(&tg, el, g2, r, 2 * r_pad, 2 * r_pad * 2, kBK, plan.sb.bn, true);
         if (e != cudaSuccess) return e;
         TcParams p{};
         p.M = d_out; p.N = r; p.k_total = 2 * r_pad;
         p.kb_per_split = static_cast<int>(2 * r_pad / kBK);
         p.n_split = plan.sb.ns; p.bn = plan.sb.bn; p.stages = stages_for(plan.sb.bn);
         p.x_kwrap = static_cast<int>(r_pad); p.chunk = a.chunk_size;
-        p.Z = static_cast<const __nv_bfloat16*>(a.b); p.ldz = r;
+        p.Z = a.b; p.ldz = r;
         p.out = ba; p.do_chain = 0;
+        p.out_scale = inv_scale;
         p.tiles = static_cast<int>(m_tiles * plan.sb.ns);
         e = launch_tc(kTcRowdot, tb, tg, p, dim3(std::max(1, plan.b_ctas), 1), vs, "ba_rowdot_tc",
-                      tpc && vs != st);
+                      tpc && vs != st, el);
         if (e == cudaSuccess && launches) ++*launches;
         return e;
     };
@@ -1264,7 +1341,7 @@ cudaError_t launch_norm_tc_f32(const NormArgs& a, Workspace* ws, cudaStream_t st
         p.bn = kBM; p.stages = stages_for(kBM, true); p.chunk = a.chunk_size;
         p.out = gpart; p.gram_nt = nt; p.tiles = gtiles;
         const int gx = std::min(gtiles, std::max(1, sms / gks));
-        if ((err = launch_tc(kTcStore, ta, ta, p, dim3(gx, gks), st, "gram_tf32x3", false, true)) != cudaSuccess)
+        if ((err = launch_tc(kTcStore, ta, ta, p, dim3(gx, gks), st, "gram_tf32x3", false, kF32)) != cudaSuccess)
             return err;
         prof_begin("gram_reduce", st);
         gram_reduce<<<static_cast<unsigned>((r * r + 255) / 256), 256, 0, st>>>(gpart, gks, nt, r, r,
@@ -1283,7 +1360,7 @@ cudaError_t launch_norm_tc_f32(const NormArgs& a, Workspace* ws, cudaStream_t st
         p.Z = a.b; p.ldz = r; p.out = cross; p.base_out = base; p.do_chain = 1;
         p.tiles = static_cast<int>(m_tiles * sp.ns);
         const int gx = std::min<int>(p.tiles, std::max(1, sms / uks));
-        if ((err = launch_tc(kTcRowdot, tw, ta, p, dim3(gx, uks), st, "u_rowdot_tf32x3", false, true)) != cudaSuccess)
+        if ((err = launch_tc(kTcRowdot, tw, ta, p, dim3(gx, uks), st, "u_rowdot_tf32x3", false, kF32)) != cudaSuccess)
             return err;
     }
     // V = B G, ba_sq = rowdot(V, B)
@@ -1297,7 +1374,7 @@ cudaError_t launch_norm_tc_f32(const NormArgs& a, Workspace* ws, cudaStream_t st
         p.Z = a.b; p.ldz = r; p.out = ba; p.do_chain = 0;
         p.tiles = static_cast<int>(m_tiles * sb.ns);
         if ((err = launch_tc(kTcRowdot, tb, tg, p, dim3(std::min(p.tiles, sms), 1), st, "ba_rowdot_tf32x3",
-                             false, true)) != cudaSuccess)
+                             false, kF32)) != cudaSuccess)
             return err;
     }
     if (launches) *launches += 5;
@@ -1335,24 +1412,37 @@ cudaError_t launch_norm_finish_tc(const NormArgs& a, Workspace* ws, cudaStream_t
         float* ba = static_cast<float*>(ws_get(ws, kWsBa, size_t(sb.ns) * d_out * sizeof(float), &err));
         if (err != cudaSuccess) return err;
         const int64_t n = r * r_pad;
+        const bool half = a.dt == kF16;
+        float* inv_scale = nullptr;
+        if (half) {
+            inv_scale = static_cast<float*>(ws_get(ws, kWsScale, 256, &err));
+            if (err != cudaSuccess) return err;
+        }
         prof_begin("gram_split", st);
-        gram_split<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(a.gram_in, r, r_pad, g2);
+        if (half)
+            gram_split<__half><<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+                a.gram_in, r, r_pad, reinterpret_cast<__half*>(g2), inv_scale);
+        else
+            gram_split<__nv_bfloat16><<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+                a.gram_in, r, r_pad, g2, nullptr);
         prof_end(st);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
         CUtensorMap tb, tg;
-        err = make_tmap_2d(&tb, kBF16, a.b, d_out, r, r * 2, kBK, kBM, true);
+        err = make_tmap_2d(&tb, a.dt, a.b, d_out, r, r * 2, kBK, kBM, true);
         if (err != cudaSuccess) return err;
-        err = make_tmap_2d(&tg, kBF16, g2, r, 2 * r_pad, 2 * r_pad * 2, kBK, sb.bn, true);
+        err = make_tmap_2d(&tg, a.dt, g2, r, 2 * r_pad, 2 * r_pad * 2, kBK, sb.bn, true);
         if (err != cudaSuccess) return err;
         TcParams p{};
         p.M = d_out; p.N = r; p.k_total = 2 * r_pad;
         p.kb_per_split = static_cast<int>(2 * r_pad / kBK);
         p.n_split = sb.ns; p.bn = sb.bn; p.stages = stages_for(sb.bn);
         p.x_kwrap = static_cast<int>(r_pad); p.chunk = 64;
-        p.Z = static_cast<const __nv_bfloat16*>(a.b); p.ldz = r;
+        p.Z = a.b; p.ldz = r;
         p.out = ba; p.do_chain = 0;
+        p.out_scale = inv_scale;
         p.tiles = static_cast<int>(m_tiles * sb.ns);
-        err = launch_tc(kTcRowdot, tb, tg, p, dim3(std::min(p.tiles, sms), 1), st, "ba_rowdot_tc");
+        err = launch_tc(kTcRowdot, tb, tg, p, dim3(std::min(p.tiles, sms), 1), st, "ba_rowdot_tc",
+                        false, a.dt);
         if (err != cudaSuccess) return err;
         if (launches) *launches += 2;
         f.cross_part = a.cross_in; f.cross_parts = 1;

@@ -14,10 +14,18 @@ Three ways the path spreads over the GPUs of one box:
   d_out=8192), and every rank finishes locally (`dfx_norm_finish`: ba_sq = rowquad(B, G),
   assemble, round, magnitude).
 
-The collective goes through torch.distributed (NCCL over NVLink on GPUs; gloo in the CPU
-tests).  K slices are aligned to the ChunkPlan so that each rank's base_sq chain covers
-whole chunks; with two ranks the reduced base_sq is then bitwise the reference's
-`base_sq += partial` over chunks (factored_norm.cpp:52-60).
+The exchange runs either as the library's own symmetric-memory kernel
+(`SymmetricAllReduce` over `dfx_norm_allreduce`: every rank reads every peer's partials over
+NVLink and sums them in rank order, one launch, no host synchronisation) or through
+torch.distributed (NCCL on GPUs; gloo, staged through host memory, in the tests).
+
+K slices are aligned to the ChunkPlan so that each rank's base_sq chain covers whole chunks.
+A rank's base_sq partial is the ascending-order sum of its chunks' serial partials, and the
+exchange adds the ranks' partials in rank order, so the reduced base_sq is bitwise the
+reference's `base_sq += partial` over chunks (factored_norm.cpp:52-60) exactly when every
+rank after the first owns ONE chunk (e.g. two ranks, the second holding the last chunk);
+otherwise fp32 addition is regrouped ((p0+p1)+(p2+p3) vs ((p0+p1)+p2)+p3) and base_sq agrees
+to fp32 rounding (tests/test_gpu_dsplit.py checks both cases).
 """
 from __future__ import annotations
 
@@ -90,18 +98,74 @@ def dsplit_bounds(d_in: int, world: int, chunk_size: int) -> List[Tuple[int, int
     return out
 
 
+class SymmetricAllReduce:
+    """The d_in split's exchange as one kernel over peer memory (include/dfx.h, dfx_comm_*).
+
+    Each rank allocates a symmetric buffer of `count` fp32 through its Dfx context, the ranks
+    swap CUDA IPC handles once through the process group (all_gather_object) and map each
+    other's buffers; `buffer()` is where this rank writes its partial terms and
+    `all_reduce(out)` writes the rank-order sum of all ranks' buffers into `out` (identical bits
+    on every rank).  Without an initialised process group (one rank) it is a copy."""
+
+    def __init__(self, dfx, count: int, group=None):
+        import torch.distributed as tdist
+        self.dist = tdist if (tdist.is_available() and tdist.is_initialized()) else None
+        self.group = group
+        self.rank = self.dist.get_rank(group) if self.dist else 0
+        self.world = self.dist.get_world_size(group) if self.dist else 1
+        self.count = count
+        self.comm = dfx.comm(self.rank, self.world, count)
+        if self.world > 1:
+            handles = [None] * self.world
+            self.dist.all_gather_object(handles, self.comm.ipc_handle(), group=group)
+            self.comm.open(handles)
+            self.dist.barrier(group=group)
+
+    def buffer(self):
+        return self.comm.buffer()
+
+    def all_reduce(self, out, stream=None):
+        self.comm.all_reduce(out, count=out.numel(), stream=stream)
+
+    def status(self) -> int:
+        return self.comm.status()
+
+    def close(self):
+        if self.comm is not None:
+            if self.world > 1:
+                self.dist.barrier(group=self.group)   # no peer still reads our buffer
+            self.comm.close()
+            self.comm = None
+
+
 def row_norm_dsplit(dfx, W_k, A_k, B, s: float, chunk_size: int, w_norm, m=None, g=None,
-                    terms=None, group=None):
+                    terms=None, group=None, comm: "SymmetricAllReduce" = None):
     """d_in-split factored norm on this rank: partial terms -> one all-reduce -> finish.
-    W_k / A_k are this rank's K columns (contiguous), B and m are replicated."""
+    W_k / A_k are this rank's K columns (contiguous), B and m are replicated.  With `comm`
+    the exchange is the library's symmetric-memory kernel; otherwise torch.distributed's
+    all_reduce (staged through host memory when the group's backend is gloo).  Returns the
+    reduced {G, base_sq, cross} buffer."""
     import torch
     import torch.distributed as tdist
 
     d_out, r = B.shape
-    buf = torch.empty(r * r + 2 * d_out, dtype=torch.float32, device=B.device)
-    gram, base, cross = buf[: r * r], buf[r * r: r * r + d_out], buf[r * r + d_out:]
-    dfx.norm_partial(W_k, A_k, B, chunk_size, gram, base, cross)
-    if tdist.is_available() and tdist.is_initialized():
-        tdist.all_reduce(buf, op=tdist.ReduceOp.SUM, group=group)
-    dfx.norm_finish(B, gram, base, cross, s, w_norm, m=m, g=g, terms=terms)
-    return buf
+    n = r * r + 2 * d_out
+    buf = comm.buffer()[:n] if comm is not None else torch.empty(n, dtype=torch.float32,
+                                                                  device=B.device)
+    dfx.norm_partial(W_k, A_k, B, chunk_size, buf[: r * r], buf[r * r: r * r + d_out],
+                     buf[r * r + d_out:])
+    if comm is not None:
+        red = torch.empty(n, dtype=torch.float32, device=B.device)
+        comm.all_reduce(red)
+    else:
+        red = buf
+        if tdist.is_available() and tdist.is_initialized():
+            if tdist.get_backend(group) == "gloo":
+                host = buf.cpu()
+                tdist.all_reduce(host, op=tdist.ReduceOp.SUM, group=group)
+                red.copy_(host)
+            else:
+                tdist.all_reduce(red, op=tdist.ReduceOp.SUM, group=group)
+    dfx.norm_finish(B, red[: r * r], red[r * r: r * r + d_out], red[r * r + d_out:], s, w_norm,
+                    m=m, g=g, terms=terms)
+    return red

@@ -23,7 +23,8 @@ def test_algorithmic_model_c2():
 
 def test_reference_arm_json(reference):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                          "--config", "c1", "--steps", "1", "--warmup", "0"],
+                          "--config", "c1", "--steps", "1", "--warmup", "0",
+                          "--no-cpu-full-module"],
                          capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
@@ -34,12 +35,19 @@ def test_reference_arm_json(reference):
     assert line["config"]["mode"] == "train"
 
 
-def test_reference_arm_stack_is_unavailable():
-    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                          "--config", "c5"], capture_output=True, text=True, timeout=120, cwd=ROOT)
-    assert out.returncode == 0
-    line = json.loads(out.stdout.strip().splitlines()[-1])
-    assert line["impl"] == "reference" and "unavailable" in line
+def test_gpus_flag_self_launches_ranks():
+    """`bench.py --gpus 2` without torchrun re-execs itself under torch.distributed.run: two
+    ranks rendezvous on 127.0.0.1, reduce their timings (max) and rank 0 reports n_gpus 2.
+    --stub swaps the GPU work for a CPU loop on gloo (this box has no GPU)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--stub",
+                          "--steps", "5"], capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["ranks_reporting"] == 2 and line["stub"] is True
 
 
 def test_reference_arm_nonzero_rank_exits_quietly():

@@ -1,7 +1,7 @@
-"""CPU tests of the multi-GPU host logic: LPT module sharding, chunk-aligned d_in split,
-and the d_in-split exchange itself over a real world_size-2 gloo process group (each rank
-computes its K-slice terms with the CPU oracle, one all-reduce of the packed
-{G, base_sq, cross} buffer, local finish) checked against the oracle's full-matrix norm."""
+"""CPU tests of the multi-GPU host logic: LPT module sharding, chunk-aligned d_in split, and
+dist.row_norm_dsplit's exchange over a real world_size-2 gloo process group (the two kernel
+calls replaced by an oracle stand-in on this GPU-less box; the product runs the same helper
+in tests/test_gpu_dist.py), checked against the oracle's full-matrix norm."""
 import os
 import socket
 import sys
@@ -62,6 +62,34 @@ def _free_port():
         return s.getsockname()[1]
 
 
+class _OracleKernels:
+    """CPU stand-in for the two Dfx calls row_norm_dsplit makes (norm_partial / norm_finish),
+    computed with the oracle, so the helper's host logic — packed {G, base_sq, cross} layout,
+    the gloo host-staged all-reduce, the finish from the reduced buffer — runs over a real
+    world-2 process group on this GPU-less box.  The product itself runs the same helper in
+    tests/test_gpu_dist.py (two processes on the GPU, gloo and the symmetric-memory kernel)."""
+
+    def __init__(self, o):
+        self.o = o
+
+    def norm_partial(self, Wk, Ak, B, cs, gram, base, cross):
+        Wk, Ak, B = (t.numpy() for t in (Wk, Ak, B))
+        base_k, cross_k, _ = self.o.norm_terms(Wk, Ak, B, 1.0, cs)     # slice chain + cross
+        gram.copy_(torch.from_numpy(
+            (Ak.astype(np.float64) @ Ak.T.astype(np.float64)).astype(np.float32).ravel()))
+        base.copy_(torch.from_numpy(base_k))
+        cross.copy_(torch.from_numpy(cross_k))
+
+    def norm_finish(self, B, gram, base, cross, s, w_norm, m=None, g=None, terms=None):
+        r = B.shape[1]
+        Bn = B.numpy().astype(np.float64)
+        G = gram.numpy().reshape(r, r).astype(np.float64)
+        ba = np.einsum("jl,lq,jq->j", Bn, G, Bn).astype(np.float32)
+        w_norm.copy_(torch.from_numpy(self.o.assemble(np.ascontiguousarray(base.numpy()),
+                                                      np.ascontiguousarray(cross.numpy()),
+                                                      ba, 2 * s, s * s)))
+
+
 def _dsplit_worker(rank, world, port, d_out, d_in, r, s, cs, out_q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -71,15 +99,12 @@ def _dsplit_worker(rank, world, port, d_out, d_in, r, s, cs, out_q):
     A = o.seeded_gaussian(r, d_in, 12)
     B = o.seeded_gaussian(d_out, r, 13)
     k0, k1 = D.dsplit_bounds(d_in, world, cs)[rank]
-    Wk, Ak = np.ascontiguousarray(W[:, k0:k1]), np.ascontiguousarray(A[:, k0:k1])
-    base_k, cross_k, _ = o.norm_terms(Wk, Ak, B, s, cs)            # slice chain + cross
-    gram_k = (Ak.astype(np.float64) @ Ak.T.astype(np.float64)).astype(np.float32)
-    buf = torch.from_numpy(np.concatenate([gram_k.ravel(), base_k, cross_k]).astype(np.float32))
-    dist.all_reduce(buf, op=dist.ReduceOp.SUM)                     # the one exchange
-    G = buf[: r * r].numpy().reshape(r, r).astype(np.float64)
-    base, cross = buf[r * r: r * r + d_out].numpy(), buf[r * r + d_out:].numpy()
-    ba = np.einsum("jl,lq,jq->j", B.astype(np.float64), G, B.astype(np.float64)).astype(np.float32)
-    norm = o.assemble(np.ascontiguousarray(base), np.ascontiguousarray(cross), ba, 2 * s, s * s)
+    Wk = torch.from_numpy(np.ascontiguousarray(W[:, k0:k1]))
+    Ak = torch.from_numpy(np.ascontiguousarray(A[:, k0:k1]))
+    wn = torch.empty(d_out)
+    red = D.row_norm_dsplit(_OracleKernels(o), Wk, Ak, torch.from_numpy(B), s, cs, wn)
+    norm = wn.numpy()
+    base = red[r * r: r * r + d_out].numpy()
     if rank == 0:
         want = o.row_norm(0, W, A, B, s, cs)
         f64 = o.dense_row_norm_f64(W, A, B, s)

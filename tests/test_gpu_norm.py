@@ -119,31 +119,51 @@ def test_base_sq_bitwise_fp32(dfx, oracle, d_out, d_in, r, cs):
     np.testing.assert_allclose(got[2], want[2], rtol=1e-4, atol=1e-4 * np.abs(want[2]).max())
 
 
+@pytest.mark.parametrize("dt", [1, 2])
 @pytest.mark.parametrize("d_out,d_in,r", [(256, 512, 64), (1024, 1024, 384), (300, 640, 40),
                                           (128, 4096, 512), (1000, 2048, 128), (8192, 256, 16),
                                           (512, 8192, 1024)])
-def test_bf16_tensor_core_path(dfx, oracle, d_out, d_in, r):
-    """tcgen05/TMA path: base_sq bitwise; cross/ba_sq vs the oracle's fp32 terms; the
-    dtype-rounded norm within one bf16 ulp of the reference's and 1e-2 of fp64."""
-    assert dfx.uses_tensor_cores(1, d_out, d_in, r)
-    W, A, B = _fixture(oracle, d_out, d_in, r, 31 * d_out + r, dt=1)
+def test_tensor_core_path(dfx, oracle, d_out, d_in, r, dt):
+    """tcgen05/TMA path, bf16 (kind::f16 with bf16 operands) and fp16 (kind::f16 with fp16
+    operands, DTypeKind::FP16E, dtype.hpp:12): base_sq bitwise; cross/ba_sq vs the oracle's fp32
+    terms; the dtype-rounded norm within one ulp of the working dtype of the reference's and
+    within the reference's bar of fp64 (1e-2 bf16, 2e-3 fp16)."""
+    assert dfx.uses_tensor_cores(dt, d_out, d_in, r)
+    W, A, B = _fixture(oracle, d_out, d_in, r, 31 * d_out + r, dt=dt)
     s = 2.0 / np.sqrt(r)
     cs, _ = oracle.plan_chunks(d_out, d_in)
     want = oracle.norm_terms(W, A, B, s, cs)
     m = np.abs(oracle.gaussian_vector(d_out, 1.0, 0.1, 5))
-    wn, g, t = _row_norm(dfx, W, A, B, s, cs, 1, m=m)
+    wn, g, t = _row_norm(dfx, W, A, B, s, cs, dt, m=m)
     assert bits_equal(t[0], want[0])
     scale_c = np.sqrt(want[0] * np.abs(want[2])) + 1e-30       # Cauchy-Schwarz size of cross
     assert np.all(np.abs(t[1] - want[1]) <= 2e-5 * scale_c + 1e-6 * np.abs(want[1]))
     assert np.all(np.abs(t[2] - want[2]) <= 1e-4 * np.abs(want[2]) + 1e-6 * want[2].max())
-    want_n = oracle.row_norm(1, W, A, B, s, cs)
-    ulp = np.spacing(want_n.astype(np.float32)) * 2 ** 16     # bf16 ulp at each value
+    want_n = oracle.row_norm(dt, W, A, B, s, cs)
+    ulp = np.spacing(want_n.astype(np.float32)) * (2 ** 16 if dt == 1 else 2 ** 13)
     assert np.all(np.abs(wn - want_n) <= ulp)
-    want_g = oracle.magnitude_scale(1, m, wn)                  # g given OUR norm: bitwise
+    want_g = oracle.magnitude_scale(dt, m, wn)                 # g given OUR norm: bitwise
     assert bits_equal(g, want_g)
     if d_out * d_in * r <= 2 ** 28:
         f64 = oracle.dense_row_norm_f64(W, A, B, s)
-        assert np.max(np.abs(wn - f64) / f64) <= 1e-2
+        assert np.max(np.abs(wn - f64) / f64) <= (1e-2 if dt == 1 else 2e-3)
+
+
+@pytest.mark.parametrize("a_scale", [1e-3, 1.0, 40.0])
+def test_fp16_gram_range(dfx, oracle, a_scale):
+    """fp16 operands: the Gram A.A^T exceeds fp16's range at large A (diag ~ d_in * 1600 here)
+    and underflows it at small A; the V GEMM's operand is G scaled by a power of two chosen
+    from its diagonal (gram_split), undone exactly in the epilogue.  ba_sq keeps the fp32 bar."""
+    d_out, d_in, r = 512, 4096, 128
+    W, A, B = _fixture(oracle, d_out, d_in, r, 77, dt=2)
+    A = (A * np.float32(a_scale)).astype(np.float16).astype(np.float32)
+    s = 2.0 / np.sqrt(r)
+    cs, _ = oracle.plan_chunks(d_out, d_in)
+    want = oracle.norm_terms(W, A, B, s, cs)
+    _, _, t = _row_norm(dfx, W, A, B, s, cs, 2)
+    assert bits_equal(t[0], want[0])
+    assert np.all(np.isfinite(t[2]))
+    assert np.all(np.abs(t[2] - want[2]) <= 1e-4 * np.abs(want[2]) + 1e-6 * want[2].max())
 
 
 def test_full_size_c2_sampled_rows(dfx, oracle):
@@ -378,11 +398,9 @@ def test_row_norm_cached_rejects(dfx):
     W = torch.zeros(256, 512, device="cuda")
     A, B = torch.zeros(16, 512, device="cuda"), torch.zeros(256, 16, device="cuda")
     c, wn = torch.zeros(256, device="cuda"), torch.zeros(256, device="cuda")
-    with pytest.raises(P.DfxError):      # fp32: not the bf16/fp16 tensor-core path
+    with pytest.raises(P.DfxError):      # fp32: not the bf16 / fp16 tensor-core path
         dfx.row_norm_cached(W, A, B, 0.5, 512, c, wn)
     Wb, Ab, Bb = W.bfloat16(), A.bfloat16(), B.bfloat16()
-    with pytest.raises(P.DfxError):      # fp16: the norm's tensor-core kernels are bf16
-        dfx.row_norm_cached(W.half(), A.half(), B.half(), 0.5, 512, c, wn)
     with pytest.raises(P.DfxError):      # s == 0 has no cross term to compute
         dfx.row_norm_cached(Wb, Ab, Bb, 0.0, 512, c, wn)
     with pytest.raises(P.DfxInvalidArgument):
@@ -401,4 +419,69 @@ def test_norm_plan_reports_budget():
         assert u <= u_all
     with pytest.raises(P.DfxError):
         dfx.norm_plan(8192, 8192, 384, 8192, dtype=P.F32)
+    dfx.close()
+
+
+def _full_size_check(dfx, oracle, d_out, d_in, r, seed, n_rows=256, cs=None):
+    """Full-size bf16 tensor-core norm: base_sq bitwise on EVERY row against the serial chunked
+    chain; cross / ba_sq on n_rows sampled rows within the Cauchy-Schwarz fp32 bounds; the
+    norm on those rows within one bf16 ulp of the reference's (oracle.row_norm)."""
+    rng = np.random.default_rng(seed)
+    W = to_np(to_dev(rng.standard_normal((d_out, d_in), dtype=np.float32), 1))
+    A = to_np(to_dev(rng.standard_normal((r, d_in), dtype=np.float32), 1))
+    B = to_np(to_dev(rng.standard_normal((d_out, r), dtype=np.float32), 1))
+    s = 2.0 / np.sqrt(r)
+    if cs is None:
+        cs, _ = oracle.plan_chunks(d_out, d_in)
+    assert dfx.uses_tensor_cores(1, d_out, d_in, r)
+    wn, _, t = _row_norm(dfx, W, A, B, s, cs, 1)
+    assert bits_equal(t[0], oracle.norm_terms(W, A, B, 0.0, cs)[0])      # s = 0: chain only
+    rows = np.sort(rng.choice(d_out, n_rows, replace=False))
+    Ws, Bs = np.ascontiguousarray(W[rows]), np.ascontiguousarray(B[rows])
+    sub = oracle.norm_terms(Ws, A, Bs, s, cs)
+    assert np.all(np.abs(t[1][rows] - sub[1]) <= 2e-5 * np.sqrt(sub[0] * sub[2]) + 1e-6 * np.abs(sub[1]))
+    assert np.all(np.abs(t[2][rows] - sub[2]) <= 1e-4 * sub[2])
+    want_n = oracle.row_norm(1, Ws, A, Bs, s, cs)
+    assert np.all(np.abs(wn[rows] - want_n) <= np.spacing(want_n.astype(np.float32)) * 2 ** 16)
+    return cs
+
+
+@pytest.mark.parametrize("budget", [0, 104])
+def test_full_size_c3_four_chunks(oracle, budget):
+    """BASELINE C3 (d_out = 28672, d_in = 8192, r = 384, bf16) at full size with the reference's
+    own plan (2304, 4): K splits only on chunk boundaries, the base_sq chain reset every 2304
+    columns, and the planner's pair tiling for this shape (full-r nh = 2 pairs and N-split
+    pairs, depending on the SM budget)."""
+    import paper_2603_22276_b200 as P
+    dfx = P.Dfx(0)
+    dfx.set_sm_budget(budget)
+    cs, nc = oracle.plan_chunks(28672, 8192)
+    assert (cs, nc) == (2304, 4)
+    assert _full_size_check(dfx, oracle, 28672, 8192, 384, 28672 + budget) == 2304
+    dfx.close()
+
+
+@pytest.mark.parametrize("r", [64, 128, 512])
+def test_full_size_c4_ranks(dfx, oracle, r):
+    """BASELINE C4 high-rank sweep at d_out = d_in = 8192 (r = 384 is C2, r = 1024 is covered by
+    test_bf16_tensor_core_path on 512 rows and the full-size sampled check below)."""
+    _full_size_check(dfx, oracle, 8192, 8192, r, 8192 + r)
+
+
+def test_full_size_c4_r1024(dfx, oracle):
+    _full_size_check(dfx, oracle, 8192, 8192, 1024, 1024, n_rows=128)
+
+
+@pytest.mark.parametrize("budget", [0, 40])
+@pytest.mark.parametrize("d_out,d_in,r,cs", [(300, 4096, 96, 1024),     # 4 chunks
+                                             (520, 6912, 384, 2304),    # 3 chunks (C3's cs)
+                                             (256, 8192, 128, 1280),    # 6 + ragged last chunk
+                                             (1000, 4608, 384, 768)])   # 6 chunks, ragged rows
+def test_bf16_multi_chunk(oracle, budget, d_out, d_in, r, cs):
+    """bf16 tensor-core norm with >= 3 ChunkPlan chunks at small d_out (explicit chunk sizes):
+    base_sq is the reference's chunked chain bitwise (factored_norm.cpp:49-101)."""
+    import paper_2603_22276_b200 as P
+    dfx = P.Dfx(0)
+    dfx.set_sm_budget(budget)
+    _full_size_check(dfx, oracle, d_out, d_in, r, d_out + cs + budget, n_rows=min(d_out, 256), cs=cs)
     dfx.close()

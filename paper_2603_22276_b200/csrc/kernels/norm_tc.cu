@@ -62,7 +62,33 @@ struct TcParams {
     int w_prefetch;         // K blocks of X (W) prefetched into L2 ahead of the loads
     int nh;                 // pair kernel: UMMAs per K step (N per CTA pair = nh * bn)
     const float* out_scale; // rowdot: multiply each row's sum by *out_scale (fp16 V: 2^-e)
+    int commit_every;       // stages per tcgen05.commit release group (see kRel)
+    int z_prefetch;         // pair rowdot: warm L2 with the tile's Z (B) rows at tile start
 };
+
+// Stage release in commit groups.  Every tcgen05.commit costs the tensor pipe ~500 cycles
+// (tools/mma_ts_micro.cu: a 2-SM N=192 UMMA costs 219 cycles at one commit per 4 UMMAs,
+// 136 per 8, 109 per 16 and reaches its 96-cycle floor at 32), so the MMA issuer commits
+// once per `commit_every` consecutive stages onto a ring of kRel release barriers and the
+// producer refills stage j only after the commit that covers fill j - stages.  The base_sq
+// chain keeps its per-stage `empty` barriers (two arrivals: chain warps or stand-ins).
+constexpr int kRel = 8;
+
+// -DDFX_TRACE (experiment builds only, scripts/build_variant.sh): the pair kernel stamps
+// %globaltimer at each pipeline event of its first kTrN stages into g_trace[cta][ev][i]
+// and the launcher dumps it to $DFX_TRACE after the launch (analysis: scripts/trace_u.py).
+#ifdef DFX_TRACE
+constexpr int kTrN = 256, kTrEv = 4, kTrCta = 148;
+__device__ unsigned long long g_trace[kTrCta][kTrEv][kTrN];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define DFX_TR(ev, i) do { if ((i) < kTrN && blockIdx.x < kTrCta) g_trace[blockIdx.x][ev][i] = gtimer(); } while (0)
+#else
+#define DFX_TR(ev, i) do { } while (0)
+#endif
 
 __device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -180,6 +206,7 @@ __device__ __forceinline__ void chain_tile(const ChainUnits& cu, const uint8_t* 
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
+        if (lane == 0 && cu.u[0] == 0) DFX_TR(3, start + it);
         kpos += kIsF32 ? 32 : 64;
         if (++s == stages) { s = 0; ph ^= 1; }
     }
@@ -229,7 +256,9 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
     uint64_t* tmem_full = empty + p.stages;     // [2]
     uint64_t* tmem_empty = tmem_full + 2;       // [2]
     uint64_t* split = tmem_empty + 2;           // [stages] (kIsF32: low parts written)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(split + p.stages);
+    uint64_t* rel = split + p.stages;           // [kRel] commit-group releases
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rel + kRel);
+    const int cg = p.commit_every > 0 ? p.commit_every : 1;
 
     const int warp = warp_id(), lane = lane_id();
     const int ks = blockIdx.y;
@@ -250,13 +279,14 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
         tma_prefetch_desc(&tmy);
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1 + (do_chain ? 2 : 0));
+            mbar_init(&empty[s], 2);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tmem_full[a], 1);
             mbar_init(&tmem_empty[a], 4);
         }
         for (int s = 0; s < p.stages; ++s) mbar_init(&split[s], kSplitWarps);
+        for (int k = 0; k < kRel; ++k) mbar_init(&rel[k], 1);
         fence_mbar_init();
     }
     if (warp == kWarpMma) {
@@ -280,7 +310,7 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
                                        ? policy_evict_first()
                                        : policy_evict_last();
             const uint64_t pol_y = policy_evict_last();
-            int s = 0;
+            int s = 0, j = 0;
             uint32_t ph = 0;
             const int pf = p.w_prefetch;
             for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
@@ -288,10 +318,14 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
                 tile_coords(kMode, p, t, m0, n0);
                 for (int it = 0; it < pf && it < nkb; ++it)
                     tma_prefetch_2d(&tmx, (kb0 + it) * kBK, static_cast<int32_t>(m0));
-                for (int it = 0; it < nkb; ++it) {
+                for (int it = 0; it < nkb; ++it, ++j) {
                     if (it + pf < nkb)
                         tma_prefetch_2d(&tmx, (kb0 + it + pf) * kBK, static_cast<int32_t>(m0));
-                    mbar_wait(&empty[s], ph ^ 1);
+                    if (j >= p.stages) {
+                        const int k = (j - p.stages) / cg;
+                        mbar_wait(&rel[k % kRel], static_cast<uint32_t>((k / kRel) & 1));
+                    }
+                    if (do_chain) mbar_wait(&empty[s], ph ^ 1);
                     mbar_arrive_expect_tx(&full[s], raw_bytes);
                     uint8_t* sx = smem + s * stage_bytes;
                     uint8_t* sy = sx + kXStage;
@@ -308,7 +342,7 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
         if (lane == 0) {
             const uint32_t idesc = kIsF32 ? umma_idesc_tf32(kBM, static_cast<uint32_t>(p.bn))
                                         : umma_idesc_f16(ab_fmt(kEl), kBM, static_cast<uint32_t>(p.bn));
-            int s = 0;
+            int s = 0, i = 0;
             uint32_t ph = 0;
             int local = 0;
             for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++local) {
@@ -338,7 +372,8 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
                             umma_f16(tacc, ad, bd, idesc, (it > 0 || k > 0) ? 1u : 0u);
                         }
                     }
-                    umma_commit(&empty[s]);
+                    if ((i + 1) % cg == 0) umma_commit(&rel[(i / cg) % kRel]);
+                    ++i;
                     // stand in for the epilogue warps that do not chain in this tile
                     if (stand_in) mbar_arrive_cnt(&empty[s], stand_in);
                     if (++s == p.stages) { s = 0; ph ^= 1; }
@@ -510,7 +545,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty = pfull + p.stages;
     uint64_t* tmem_full = empty + p.stages;     // [2]
     uint64_t* tmem_empty = tmem_full + 2;       // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    uint64_t* rel = tmem_empty + 2;             // [kRel] commit-group releases (both CTAs)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rel + kRel);
+    const int cg = p.commit_every > 0 ? p.commit_every : 1;
 
     const int warp = warp_id(), lane = lane_id();
     const uint32_t rank = cluster_ctarank();
@@ -535,12 +572,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&pfull[s], 1);
-            mbar_init(&empty[s], 1 + (do_chain ? 2 : 0));
+            mbar_init(&empty[s], 2);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tmem_full[a], 1);
             mbar_init(&tmem_empty[a], 8);
         }
+        for (int k = 0; k < kRel; ++k) mbar_init(&rel[k], 1);
         fence_mbar_init();
     }
     if (warp == kWarpMma) {
@@ -563,19 +601,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             const uint64_t pol_x = p.n_split == 1 ? policy_evict_first() : policy_evict_last();
             const uint64_t pol_y = policy_evict_last();
-            int s = 0;
+            int s = 0, j = 0;
             uint32_t ph = 0;
             const int pf = p.w_prefetch;
             for (int t = pair; t < p.tiles; t += npairs) {
                 const int64_t m0 = int64_t(t / p.n_split) * (2 * kBM) + int64_t(rank) * kBM;
                 const int64_t n0 = int64_t(t % p.n_split) * bn_pair + int64_t(rank) * half_n;
+                if (p.z_prefetch) {
+                    // the epilogue reads this CTA's 128 rows x bn_pair columns of Z (B)
+                    const int64_t zc = int64_t(t % p.n_split) * bn_pair;
+                    const int64_t zn = bn_pair < p.N - zc ? int64_t(bn_pair) : p.N - zc;
+                    for (int rr = 0; rr < kBM && m0 + rr < p.M; ++rr)
+                        bulk_prefetch_l2(static_cast<const uint16_t*>(p.Z) + (m0 + rr) * p.ldz + zc,
+                                         static_cast<uint32_t>(zn * 2));
+                }
                 // W streams from HBM in 128-byte row pieces: warm L2 `pf` K blocks ahead
                 for (int it = 0; it < pf && it < nkb; ++it)
                     tma_prefetch_2d(&tmx, (kb0 + it) * kBK, static_cast<int32_t>(m0));
-                for (int it = 0; it < nkb; ++it) {
+                for (int it = 0; it < nkb; ++it, ++j) {
                     if (it + pf < nkb)
                         tma_prefetch_2d(&tmx, (kb0 + it + pf) * kBK, static_cast<int32_t>(m0));
-                    mbar_wait(&empty[s], ph ^ 1);
+                    if (j >= p.stages) {
+                        const int k = (j - p.stages) / cg;
+                        mbar_wait(&rel[k % kRel], static_cast<uint32_t>((k / kRel) & 1));
+                    }
+                    if (do_chain) mbar_wait(&empty[s], ph ^ 1);
+                    DFX_TR(0, j);
                     if (leader) mbar_arrive_expect_tx(&full[s], 2 * stage_bytes);
                     const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
                     uint8_t* sx = smem + s * stage_bytes;
@@ -593,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ================= MMA issuer (leader CTA, single thread) =================
         if (leader && lane == 0) {
             const uint32_t idesc = umma_idesc_f16(ab_fmt(kEl), 2 * kBM, static_cast<uint32_t>(p.bn));
-            int s = 0;
+            int s = 0, i = 0;
             uint32_t ph = 0;
             int local = 0;
             for (int t = pair; t < p.tiles; t += npairs, ++local) {
@@ -604,6 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 for (int it = 0; it < nkb; ++it) {
                     mbar_wait(&full[s], ph);
+                    DFX_TR(1, i);
                     tc_fence_after();
                     const uint32_t sx = smem_u32(smem + s * stage_bytes);
                     for (int h = 0; h < nh; ++h) {
@@ -620,12 +672,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
                         }
                     }
-#ifndef DFX_KO_COMMIT
-                    umma_commit_pair_mc(&empty[s], 0x3);
-#else
-                    mbar_arrive(&empty[s]);
-                    mbar_arrive_remote(mapa_shared(smem_u32(&empty[s]), 1), 1);
-#endif
+                    if ((i + 1) % cg == 0) umma_commit_pair_mc(&rel[(i / cg) % kRel], 0x3);
+                    DFX_TR(2, i);
+                    ++i;
                     if (++s == p.stages) { s = 0; ph ^= 1; }
                 }
                 umma_commit_pair_mc(&tmem_full[slot], 0x3);
@@ -794,14 +843,31 @@ __global__ void __launch_bounds__(256) gram_split(const float* __restrict__ g, i
     g2[i * 2 * r_pad + r_pad + j] = Elem<T>::from_f(__fsub_rn(v, Elem<T>::to_f(hi)));
 }
 
+constexpr int kBarBytes = 512;                   // mbarriers (<= 3 x 8 + 4 + kRel) + TMEM slot
+
 int stages_for(int bn, bool f32 = false) {
     const int stage = (kXStage + bn * kBK * 2) * (f32 ? 2 : 1);
-    const int avail = kMaxSmem - 1024 - 256;
+    const int avail = kMaxSmem - 1024 - kBarBytes;
     return std::min(8, avail / stage);
 }
 
+// Stages per commit group (TcParams::commit_every): enough UMMAs per tcgen05.commit to
+// amortise its cost (target 24, DFX_COMMIT_UMMAS overrides for measurements) while at least
+// two groups of the ring stay in flight.
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+int commit_group(int umma_per_stage, int stages) {
+    static const int target = std::max(1, env_int("DFX_COMMIT_UMMAS", 24));
+    static const int cap_div = std::max(1, env_int("DFX_COMMIT_CAPDIV", 2));
+    const int g = (target + umma_per_stage - 1) / umma_per_stage;
+    return std::max(1, std::min(g, std::max(1, stages / cap_div) - (cap_div == 1 ? 1 : 0)));
+}
+
 size_t smem_for(int bn, int stages, bool f32 = false) {
-    return size_t(stages) * (kXStage + bn * kBK * 2) * (f32 ? 2 : 1) + 1024 + 256;
+    return size_t(stages) * (kXStage + bn * kBK * 2) * (f32 ? 2 : 1) + 1024 + kBarBytes;
 }
 
 // tpc_pairs: launch as clusters of 2 so the kernel occupies whole TPCs (used for the
@@ -812,6 +878,7 @@ cudaError_t launch_tc(int mode, const CUtensorMap& tx, const CUtensorMap& ty, Tc
                       int el = kBF16) {
     const bool f32 = el == kF32;
     const size_t smem = smem_for(p.bn, p.stages, f32);
+    if (p.commit_every <= 0) p.commit_every = commit_group(f32 ? 12 : 4, p.stages);
     cudaError_t e;
     auto kern = el == kF32   ? (mode == kTcRowdot ? tc_rowdot<kTcRowdot, kF32> : tc_rowdot<kTcStore, kF32>)
                 : el == kF16 ? (mode == kTcRowdot ? tc_rowdot<kTcRowdot, kF16> : tc_rowdot<kTcStore, kF16>)
@@ -838,18 +905,22 @@ cudaError_t launch_tc(int mode, const CUtensorMap& tx, const CUtensorMap& ty, Tc
 }
 
 size_t smem_for_pair(int bn, int stages, int nh = 1) {
-    return size_t(stages) * (kXStage + nh * (bn / 2) * kBK * 2) + 1024 + 256;
+    return size_t(stages) * (kXStage + nh * (bn / 2) * kBK * 2) + 1024 + kBarBytes;
 }
 
 int stages_for_pair(int bn, int nh = 1) {
     const int stage = kXStage + nh * (bn / 2) * kBK * 2;
-    return std::min(8, (kMaxSmem - 1024 - 256) / stage);
+    return std::min(8, (kMaxSmem - 1024 - kBarBytes) / stage);
 }
 
 cudaError_t launch_tc_pair(const CUtensorMap& tx, const CUtensorMap& ty, TcParams p, int pairs,
                            int ks, cudaStream_t st, const char* name, int el) {
     cudaError_t e;
     auto kern = el == kF16 ? tc_pair_rowdot<kF16> : tc_pair_rowdot<kBF16>;
+    if (p.commit_every <= 0) p.commit_every = commit_group(4 * (p.nh > 0 ? p.nh : 1), p.stages);
+    static const int wpf = env_int("DFX_W_PREFETCH", -1), zpf = env_int("DFX_Z_PREFETCH", -1);
+    if (wpf >= 0) p.w_prefetch = wpf;
+    if (zpf >= 0) p.z_prefetch = zpf;
     if ((e = ensure_max_dyn_smem(reinterpret_cast<const void*>(kern), kMaxSmem)) != cudaSuccess)
         return e;
     cudaLaunchConfig_t cfg = {};
@@ -857,6 +928,14 @@ cudaError_t launch_tc_pair(const CUtensorMap& tx, const CUtensorMap& ty, TcParam
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem_for_pair(p.bn, p.stages, p.nh > 0 ? p.nh : 1);
     cfg.stream = st;
+#ifdef DFX_TRACE
+    const char* trace_file = std::getenv("DFX_TRACE");
+    if (trace_file) {
+        void* tp = nullptr;
+        cudaGetSymbolAddress(&tp, g_trace);
+        cudaMemsetAsync(tp, 0, sizeof(g_trace), st);
+    }
+#endif
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
@@ -868,6 +947,19 @@ cudaError_t launch_tc_pair(const CUtensorMap& tx, const CUtensorMap& ty, TcParam
     e = cudaLaunchKernelEx(&cfg, kern, tx, ty, p);
     prof_end(st);
     if (e != cudaSuccess) return e;
+#ifdef DFX_TRACE
+    if (trace_file) {
+        static unsigned long long host[kTrCta][kTrEv][kTrN];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(host, g_trace, sizeof(host));
+        if (FILE* f = std::fopen(trace_file, "ab")) {
+            const int hdr[8] = {2 * pairs, p.stages, p.kb_per_split, p.nh, p.bn, p.commit_every, p.tiles, ks};
+            std::fwrite(hdr, sizeof(hdr), 1, f);
+            std::fwrite(host, sizeof(host), 1, f);
+            std::fclose(f);
+        }
+    }
+#endif
     return cudaGetLastError();
 }
 

@@ -96,6 +96,13 @@ __device__ __forceinline__ void tma_prefetch_2d(const void* desc, int32_t c0, in
                  : "memory");
 }
 
+// Prefetch `bytes` (multiple of 16, 16-byte aligned) of global memory into L2.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gptr, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(gptr)),
+                 "r"(bytes)
+                 : "memory");
+}
+
 // L2 cache policies (createpolicy.fractional).
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;

@@ -156,38 +156,7 @@ __global__ void __launch_bounds__(256) base_chain(const T* __restrict__ W, int64
 // Sum partials in fixed (ascending) order, then assemble_norm -> round -> magnitude.
 __global__ void __launch_bounds__(256) finish_kernel(FinishArgs f) {
     const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j >= f.d_out) return;
-    float b = 0.0f, c = 0.0f, q = 0.0f;
-    if (f.base_part) {
-        b = f.base_part[j];
-        for (int p = 1; p < f.base_parts; ++p) b = __fadd_rn(b, f.base_part[p * f.d_out + j]);
-    }
-    if (f.cross_part) {
-        c = f.cross_part[j];
-        for (int p = 1; p < f.cross_parts; ++p) c = __fadd_rn(c, f.cross_part[p * f.d_out + j]);
-    }
-    if (f.ba_part) {
-        q = f.ba_part[j];
-        for (int p = 1; p < f.ba_parts; ++p) q = __fadd_rn(q, f.ba_part[p * f.d_out + j]);
-    }
-    if (f.base_sq) f.base_sq[j] = b;
-    if (f.cross) f.cross[j] = c;
-    if (f.ba_sq) f.ba_sq[j] = q;
-    if (!f.w_norm && !f.g) return;
-    // assemble_norm (factored_norm.cpp:128-134)
-    const float c1 = __double2float_rn(__dmul_rn(f.two_s, static_cast<double>(c)));
-    const float t1 = __fadd_rn(b, c1);
-    const float c2 = __double2float_rn(__dmul_rn(f.s2, static_cast<double>(q)));
-    float t2 = __fadd_rn(t1, c2);
-    t2 = (t2 < 0.0f) ? 0.0f : t2;  // NaN compares false and passes through
-    const float nrm = round_store(__fsqrt_rn(t2), f.round_dt);
-    if (f.w_norm) f.w_norm[j] = nrm;
-    if (f.g) {
-        // magnitude_scale (factored_norm.cpp:232-239)
-        const float eps = (f.mag_dt == kF32) ? static_cast<float>(1e-12) : static_cast<float>(1e-6);
-        const float denom = nrm < eps ? eps : nrm;
-        f.g[j] = round_store(__fdiv_rn(f.m[j], denom), f.mag_dt);
-    }
+    if (j < f.d_out) finish_row(f, j);
 }
 
 __global__ void __launch_bounds__(256) magnitude_kernel(const float* __restrict__ m,

@@ -61,34 +61,34 @@ struct TcParams {
     int tiles;              // tiles per K split (the persistent loop's extent)
     int w_prefetch;         // K blocks of X (W) prefetched into L2 ahead of the loads
     int nh;                 // pair kernel: UMMAs per K step (N per CTA pair = nh * bn)
+    int ka;                 // pair kernel: 64-wide K blocks ("atoms") per ring stage (1 or 2)
     const float* out_scale; // rowdot: multiply each row's sum by *out_scale (fp16 V: 2^-e)
-    int commit_every;       // stages per tcgen05.commit release group (see kRel)
-    int z_prefetch;         // pair rowdot: warm L2 with the tile's Z (B) rows at tile start
+    // Fused finisher (rowdot): every tile of a 128-row block counts itself in
+    // fin_count[block]; the tile completing the block (fin_total tiles over U and V) runs
+    // finish_row for its rows, so no separate finish launch sits on the critical path.
+    FinishArgs fin;
+    unsigned* fin_count;
+    int fin_total;
 };
 
-// Stage release in commit groups.  Every tcgen05.commit costs the tensor pipe ~500 cycles
-// (tools/mma_ts_micro.cu: a 2-SM N=192 UMMA costs 219 cycles at one commit per 4 UMMAs,
-// 136 per 8, 109 per 16 and reaches its 96-cycle floor at 32), so the MMA issuer commits
-// once per `commit_every` consecutive stages onto a ring of kRel release barriers and the
-// producer refills stage j only after the commit that covers fill j - stages.  The base_sq
-// chain keeps its per-stage `empty` barriers (two arrivals: chain warps or stand-ins).
-constexpr int kRel = 8;
-
-// -DDFX_TRACE (experiment builds only, scripts/build_variant.sh): the pair kernel stamps
-// %globaltimer at each pipeline event of its first kTrN stages into g_trace[cta][ev][i]
-// and the launcher dumps it to $DFX_TRACE after the launch (analysis: scripts/trace_u.py).
-#ifdef DFX_TRACE
-constexpr int kTrN = 256, kTrEv = 4, kTrCta = 148;
-__device__ unsigned long long g_trace[kTrCta][kTrEv][kTrN];
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
+// Epilogue warps 0..3 (128 threads) after a tile's outputs are stored: count the tile in
+// its group; true in all 128 threads of the CTA whose tile completed the group.  The last
+// arrival resets the counter, so the next launch (stream-ordered) starts from zero.
+// `flag` is a word of the CTA's barrier area (no static shared memory: the kernels use the
+// whole 227 KiB opt-in dynamically).
+__device__ __forceinline__ bool last_arrival(unsigned* count, int total, volatile uint32_t* flag) {
+    __threadfence();
+    named_bar_sync(1, 128);
+    if (threadIdx.x == 0) {
+        const bool last = atomicAdd(count, 1u) + 1u == static_cast<unsigned>(total);
+        if (last) atomicExch(count, 0u);
+        *flag = last ? 1u : 0u;
+    }
+    named_bar_sync(1, 128);
+    const bool last = *flag != 0;
+    if (last) __threadfence();
+    return last;
 }
-#define DFX_TR(ev, i) do { if ((i) < kTrN && blockIdx.x < kTrCta) g_trace[blockIdx.x][ev][i] = gtimer(); } while (0)
-#else
-#define DFX_TR(ev, i) do { } while (0)
-#endif
 
 __device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -152,7 +152,8 @@ template <int kRows, int kEl = kBF16>
 __device__ __forceinline__ void chain_tile(const ChainUnits& cu, const uint8_t* smem,
                                            int stage_bytes, uint64_t* ready, uint64_t* empty,
                                            int stages, int start, int nkb, int kb0, int64_t chunk,
-                                           int64_t m0, int64_t M, float* base_out, int lane) {
+                                           int64_t m0, int64_t M, float* base_out, int lane,
+                                           int ka = 1) {
     constexpr bool kIsF32 = kEl == kF32;
     int s = start % stages;
     uint32_t ph = static_cast<uint32_t>((start / stages) & 1);
@@ -168,10 +169,11 @@ __device__ __forceinline__ void chain_tile(const ChainUnits& cu, const uint8_t* 
     int64_t boundary = (cur + 1) * chunk;
     for (int it = 0; it < nkb; ++it) {
         mbar_wait(&ready[s], ph);
+        for (int a = 0; a < ka; ++a) {   // K atoms of the stage, ascending K (X atoms first)
         uint4 v[kRows][8];
 #pragma unroll
         for (int j = 0; j < kRows; ++j) {
-            const uint8_t* rowp = smem + s * stage_bytes + row[j] * 128;
+            const uint8_t* rowp = smem + s * stage_bytes + a * kXStage + row[j] * 128;
 #pragma unroll
             for (int c = 0; c < 8; ++c)
                 v[j][c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ (row[j] & 7)) << 4));
@@ -204,10 +206,10 @@ __device__ __forceinline__ void chain_tile(const ChainUnits& cu, const uint8_t* 
                 for (int j = 0; j < kRows; ++j)
                     part[j] = __fadd_rn(part[j], __fmul_rn(f[j][e], f[j][e]));
         }
+        kpos += kIsF32 ? 32 : 64;
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        if (lane == 0 && cu.u[0] == 0) DFX_TR(3, start + it);
-        kpos += kIsF32 ? 32 : 64;
         if (++s == stages) { s = 0; ph ^= 1; }
     }
 #pragma unroll
@@ -256,9 +258,7 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
     uint64_t* tmem_full = empty + p.stages;     // [2]
     uint64_t* tmem_empty = tmem_full + 2;       // [2]
     uint64_t* split = tmem_empty + 2;           // [stages] (kIsF32: low parts written)
-    uint64_t* rel = split + p.stages;           // [kRel] commit-group releases
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rel + kRel);
-    const int cg = p.commit_every > 0 ? p.commit_every : 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(split + p.stages);
 
     const int warp = warp_id(), lane = lane_id();
     const int ks = blockIdx.y;
@@ -279,14 +279,13 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
         tma_prefetch_desc(&tmy);
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 2);
+            mbar_init(&empty[s], 1 + (do_chain ? 2 : 0));
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tmem_full[a], 1);
             mbar_init(&tmem_empty[a], 4);
         }
         for (int s = 0; s < p.stages; ++s) mbar_init(&split[s], kSplitWarps);
-        for (int k = 0; k < kRel; ++k) mbar_init(&rel[k], 1);
         fence_mbar_init();
     }
     if (warp == kWarpMma) {
@@ -310,7 +309,7 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
                                        ? policy_evict_first()
                                        : policy_evict_last();
             const uint64_t pol_y = policy_evict_last();
-            int s = 0, j = 0;
+            int s = 0;
             uint32_t ph = 0;
             const int pf = p.w_prefetch;
             for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
@@ -318,14 +317,10 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
                 tile_coords(kMode, p, t, m0, n0);
                 for (int it = 0; it < pf && it < nkb; ++it)
                     tma_prefetch_2d(&tmx, (kb0 + it) * kBK, static_cast<int32_t>(m0));
-                for (int it = 0; it < nkb; ++it, ++j) {
+                for (int it = 0; it < nkb; ++it) {
                     if (it + pf < nkb)
                         tma_prefetch_2d(&tmx, (kb0 + it + pf) * kBK, static_cast<int32_t>(m0));
-                    if (j >= p.stages) {
-                        const int k = (j - p.stages) / cg;
-                        mbar_wait(&rel[k % kRel], static_cast<uint32_t>((k / kRel) & 1));
-                    }
-                    if (do_chain) mbar_wait(&empty[s], ph ^ 1);
+                    mbar_wait(&empty[s], ph ^ 1);
                     mbar_arrive_expect_tx(&full[s], raw_bytes);
                     uint8_t* sx = smem + s * stage_bytes;
                     uint8_t* sy = sx + kXStage;
@@ -342,7 +337,7 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
         if (lane == 0) {
             const uint32_t idesc = kIsF32 ? umma_idesc_tf32(kBM, static_cast<uint32_t>(p.bn))
                                         : umma_idesc_f16(ab_fmt(kEl), kBM, static_cast<uint32_t>(p.bn));
-            int s = 0, i = 0;
+            int s = 0;
             uint32_t ph = 0;
             int local = 0;
             for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++local) {
@@ -372,8 +367,7 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
                             umma_f16(tacc, ad, bd, idesc, (it > 0 || k > 0) ? 1u : 0u);
                         }
                     }
-                    if ((i + 1) % cg == 0) umma_commit(&rel[(i / cg) % kRel]);
-                    ++i;
+                    umma_commit(&empty[s]);
                     // stand in for the epilogue warps that do not chain in this tile
                     if (stand_in) mbar_arrive_cnt(&empty[s], stand_in);
                     if (++s == p.stages) { s = 0; ph ^= 1; }
@@ -483,6 +477,8 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
                 if (lane == 0) mbar_arrive(&tmem_empty[slot]);
                 if (p.out_scale) acc = __fmul_rn(acc, *p.out_scale);   // exact power of two
                 if (gm < p.M) p.out[(int64_t(ks) * p.n_split + (n0 / p.bn)) * p.M + gm] = acc;
+                if (p.fin_count && last_arrival(p.fin_count + m0 / kBM, p.fin_total, tmem_slot + 1) && gm < p.M)
+                    finish_row(p.fin, gm);
             } else {
                 // gram tile store: out[(ks * tiles + t) * 128*bn + row*bn + col]
                 float* dst = p.out + (int64_t(ks) * p.tiles + t) * (int64_t(kBM) * p.bn) +
@@ -537,17 +533,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                ~uintptr_t(1023));
     const int half_n = p.bn / 2;                          // A rows per CTA per UMMA
     const int nh = p.nh > 0 ? p.nh : 1;
+    const int ka = p.ka > 0 ? p.ka : 1;                   // K atoms per stage
     const int y_bytes = half_n * kBK * 2;
-    const int stage_bytes = kXStage + nh * y_bytes;       // this CTA's share of a stage
+    // this CTA's share of a stage: [X atom 0 .. ka-1 | Y (h, atom) h-major]
+    const int stage_bytes = ka * (kXStage + nh * y_bytes);
     const int bn_pair = nh * p.bn;                        // N of the pair's tile
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
     uint64_t* pfull = full + p.stages;
     uint64_t* empty = pfull + p.stages;
     uint64_t* tmem_full = empty + p.stages;     // [2]
     uint64_t* tmem_empty = tmem_full + 2;       // [2]
-    uint64_t* rel = tmem_empty + 2;             // [kRel] commit-group releases (both CTAs)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rel + kRel);
-    const int cg = p.commit_every > 0 ? p.commit_every : 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
     const int warp = warp_id(), lane = lane_id();
     const uint32_t rank = cluster_ctarank();
@@ -557,7 +553,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kb0 = ks * p.kb_per_split;
     const int64_t total_kb = (p.k_total + kBK - 1) / kBK;
     const int64_t kb_left = total_kb - kb0;
-    const int nkb = static_cast<int>(kb_left < p.kb_per_split ? kb_left : p.kb_per_split);
+    const int nkb_blocks = static_cast<int>(kb_left < p.kb_per_split ? kb_left : p.kb_per_split);
+    const int nkb = nkb_blocks / ka;             // ring stages per tile (the planner keeps ka | nkb)
     const bool do_chain = p.do_chain != 0;
 
     // accumulator slots: double-buffered when two fit in the 512 TMEM columns
@@ -572,13 +569,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&pfull[s], 1);
-            mbar_init(&empty[s], 2);
+            mbar_init(&empty[s], 1 + (do_chain ? 2 : 0));
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tmem_full[a], 1);
             mbar_init(&tmem_empty[a], 8);
         }
-        for (int k = 0; k < kRel; ++k) mbar_init(&rel[k], 1);
         fence_mbar_init();
     }
     if (warp == kWarpMma) {
@@ -601,41 +597,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             const uint64_t pol_x = p.n_split == 1 ? policy_evict_first() : policy_evict_last();
             const uint64_t pol_y = policy_evict_last();
-            int s = 0, j = 0;
+            int s = 0;
             uint32_t ph = 0;
             const int pf = p.w_prefetch;
             for (int t = pair; t < p.tiles; t += npairs) {
                 const int64_t m0 = int64_t(t / p.n_split) * (2 * kBM) + int64_t(rank) * kBM;
                 const int64_t n0 = int64_t(t % p.n_split) * bn_pair + int64_t(rank) * half_n;
-                if (p.z_prefetch) {
-                    // the epilogue reads this CTA's 128 rows x bn_pair columns of Z (B)
-                    const int64_t zc = int64_t(t % p.n_split) * bn_pair;
-                    const int64_t zn = bn_pair < p.N - zc ? int64_t(bn_pair) : p.N - zc;
-                    for (int rr = 0; rr < kBM && m0 + rr < p.M; ++rr)
-                        bulk_prefetch_l2(static_cast<const uint16_t*>(p.Z) + (m0 + rr) * p.ldz + zc,
-                                         static_cast<uint32_t>(zn * 2));
-                }
                 // W streams from HBM in 128-byte row pieces: warm L2 `pf` K blocks ahead
-                for (int it = 0; it < pf && it < nkb; ++it)
+                for (int it = 0; it < pf && it < nkb_blocks; ++it)
                     tma_prefetch_2d(&tmx, (kb0 + it) * kBK, static_cast<int32_t>(m0));
-                for (int it = 0; it < nkb; ++it, ++j) {
-                    if (it + pf < nkb)
-                        tma_prefetch_2d(&tmx, (kb0 + it + pf) * kBK, static_cast<int32_t>(m0));
-                    if (j >= p.stages) {
-                        const int k = (j - p.stages) / cg;
-                        mbar_wait(&rel[k % kRel], static_cast<uint32_t>((k / kRel) & 1));
-                    }
-                    if (do_chain) mbar_wait(&empty[s], ph ^ 1);
-                    DFX_TR(0, j);
+                for (int it = 0; it < nkb; ++it) {
+                    for (int a = 0; a < ka; ++a)
+                        if (it * ka + a + pf < nkb_blocks)
+                            tma_prefetch_2d(&tmx, (kb0 + it * ka + a + pf) * kBK, static_cast<int32_t>(m0));
+                    mbar_wait(&empty[s], ph ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[s], 2 * stage_bytes);
                     const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
                     uint8_t* sx = smem + s * stage_bytes;
-                    uint8_t* sy = sx + kXStage;
-                    const int kc = (kb0 + it) * kBK;
-                    tma_load_2d_pair(&tmx, lbar, sx, kc, static_cast<int32_t>(m0), pol_x);
-                    for (int h = 0; h < nh; ++h)
-                        tma_load_2d_pair(&tmy, lbar, sy + h * y_bytes, kc,
-                                         static_cast<int32_t>(n0 + int64_t(h) * p.bn), pol_y);
+                    uint8_t* sy = sx + ka * kXStage;
+                    for (int a = 0; a < ka; ++a) {
+                        const int kc = (kb0 + it * ka + a) * kBK;
+                        tma_load_2d_pair(&tmx, lbar, sx + a * kXStage, kc, static_cast<int32_t>(m0), pol_x);
+                        for (int h = 0; h < nh; ++h)
+                            tma_load_2d_pair(&tmy, lbar, sy + (h * ka + a) * y_bytes, kc,
+                                             static_cast<int32_t>(n0 + int64_t(h) * p.bn), pol_y);
+                    }
                     if (++s == p.stages) { s = 0; ph ^= 1; }
                 }
             }
@@ -644,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ================= MMA issuer (leader CTA, single thread) =================
         if (leader && lane == 0) {
             const uint32_t idesc = umma_idesc_f16(ab_fmt(kEl), 2 * kBM, static_cast<uint32_t>(p.bn));
-            int s = 0, i = 0;
+            int s = 0;
             uint32_t ph = 0;
             int local = 0;
             for (int t = pair; t < p.tiles; t += npairs, ++local) {
@@ -655,26 +641,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 for (int it = 0; it < nkb; ++it) {
                     mbar_wait(&full[s], ph);
-                    DFX_TR(1, i);
                     tc_fence_after();
-                    const uint32_t sx = smem_u32(smem + s * stage_bytes);
+                    const uint32_t sx0 = smem_u32(smem + s * stage_bytes);
                     for (int h = 0; h < nh; ++h) {
-                        const uint32_t sy = sx + kXStage + h * y_bytes;
+                        for (int a = 0; a < ka; ++a) {
+                            const uint32_t sx = sx0 + a * kXStage;
+                            const uint32_t sy = sx0 + ka * kXStage + (h * ka + a) * y_bytes;
 #pragma unroll
-                        for (int k = 0; k < kBK / 16; ++k) {
-                            const uint64_t ad = umma_desc_k_sw128(sx + k * 32);
-                            const uint64_t bd = umma_desc_k_sw128(sy + k * 32);
+                            for (int k = 0; k < kBK / 16; ++k) {
+                                const uint64_t ad = umma_desc_k_sw128(sx + k * 32);
+                                const uint64_t bd = umma_desc_k_sw128(sy + k * 32);
 #ifndef DFX_KO_MMA
-                            umma_f16_pair(tacc + static_cast<uint32_t>(h * p.bn), ad, bd, idesc,
-                                          (it > 0 || k > 0) ? 1u : 0u);
+                                umma_f16_pair(tacc + static_cast<uint32_t>(h * p.bn), ad, bd, idesc,
+                                              (it > 0 || a > 0 || k > 0) ? 1u : 0u);
 #else
-                            (void)ad; (void)bd;
+                                (void)ad; (void)bd;
 #endif
+                            }
                         }
                     }
-                    if ((i + 1) % cg == 0) umma_commit_pair_mc(&rel[(i / cg) % kRel], 0x3);
-                    DFX_TR(2, i);
-                    ++i;
+#ifndef DFX_KO_COMMIT
+                    umma_commit_pair_mc(&empty[s], 0x3);
+#else
+                    mbar_arrive(&empty[s]);
+                    mbar_arrive_remote(mapa_shared(smem_u32(&empty[s]), 1), 1);
+#endif
                     if (++s == p.stages) { s = 0; ph ^= 1; }
                 }
                 umma_commit_pair_mc(&tmem_full[slot], 0x3);
@@ -715,10 +706,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const ChainUnits cu = chain_units(warp, static_cast<int>(t % p.n_split), p.n_split);
                 if (cu.n == 2)
                     chain_tile<2, kEl>(cu, smem, stage_bytes, ready, empty, p.stages, local * nkb, nkb, kb0,
-                                  p.chunk, m0, p.M, p.base_out, lane);
+                                  p.chunk, m0, p.M, p.base_out, lane, ka);
                 else if (cu.n == 1)
                     chain_tile<1, kEl>(cu, smem, stage_bytes, ready, empty, p.stages, local * nkb, nkb, kb0,
-                                  p.chunk, m0, p.M, p.base_out, lane);
+                                  p.chunk, m0, p.M, p.base_out, lane, ka);
             }
             const int slot = nslots == 2 ? (local & 1) : 0;
             const int use = nslots == 2 ? (local >> 1) : local;
@@ -755,6 +746,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else mbar_arrive_remote(mapa_shared(smem_u32(&tmem_empty[slot]), 0), 1);
             }
             if (gm < p.M) p.out[(int64_t(ks) * p.n_split + (n0 / bn_pair)) * p.M + gm] = acc;
+            if (p.fin_count && last_arrival(p.fin_count + m0 / kBM, p.fin_total, tmem_slot + 1) && gm < p.M)
+                finish_row(p.fin, gm);
         }
     }
     tc_fence_before();
@@ -843,31 +836,14 @@ __global__ void __launch_bounds__(256) gram_split(const float* __restrict__ g, i
     g2[i * 2 * r_pad + r_pad + j] = Elem<T>::from_f(__fsub_rn(v, Elem<T>::to_f(hi)));
 }
 
-constexpr int kBarBytes = 512;                   // mbarriers (<= 3 x 8 + 4 + kRel) + TMEM slot
-
 int stages_for(int bn, bool f32 = false) {
     const int stage = (kXStage + bn * kBK * 2) * (f32 ? 2 : 1);
-    const int avail = kMaxSmem - 1024 - kBarBytes;
+    const int avail = kMaxSmem - 1024 - 256;
     return std::min(8, avail / stage);
 }
 
-// Stages per commit group (TcParams::commit_every): enough UMMAs per tcgen05.commit to
-// amortise its cost (target 24, DFX_COMMIT_UMMAS overrides for measurements) while at least
-// two groups of the ring stay in flight.
-int env_int(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e ? std::atoi(e) : dflt;
-}
-
-int commit_group(int umma_per_stage, int stages) {
-    static const int target = std::max(1, env_int("DFX_COMMIT_UMMAS", 24));
-    static const int cap_div = std::max(1, env_int("DFX_COMMIT_CAPDIV", 2));
-    const int g = (target + umma_per_stage - 1) / umma_per_stage;
-    return std::max(1, std::min(g, std::max(1, stages / cap_div) - (cap_div == 1 ? 1 : 0)));
-}
-
 size_t smem_for(int bn, int stages, bool f32 = false) {
-    return size_t(stages) * (kXStage + bn * kBK * 2) * (f32 ? 2 : 1) + 1024 + kBarBytes;
+    return size_t(stages) * (kXStage + bn * kBK * 2) * (f32 ? 2 : 1) + 1024 + 256;
 }
 
 // tpc_pairs: launch as clusters of 2 so the kernel occupies whole TPCs (used for the
@@ -878,7 +854,6 @@ cudaError_t launch_tc(int mode, const CUtensorMap& tx, const CUtensorMap& ty, Tc
                       int el = kBF16) {
     const bool f32 = el == kF32;
     const size_t smem = smem_for(p.bn, p.stages, f32);
-    if (p.commit_every <= 0) p.commit_every = commit_group(f32 ? 12 : 4, p.stages);
     cudaError_t e;
     auto kern = el == kF32   ? (mode == kTcRowdot ? tc_rowdot<kTcRowdot, kF32> : tc_rowdot<kTcStore, kF32>)
                 : el == kF16 ? (mode == kTcRowdot ? tc_rowdot<kTcRowdot, kF16> : tc_rowdot<kTcStore, kF16>)
@@ -904,38 +879,43 @@ cudaError_t launch_tc(int mode, const CUtensorMap& tx, const CUtensorMap& ty, Tc
     return cudaGetLastError();
 }
 
-size_t smem_for_pair(int bn, int stages, int nh = 1) {
-    return size_t(stages) * (kXStage + nh * (bn / 2) * kBK * 2) + 1024 + kBarBytes;
+size_t smem_for_pair(int bn, int stages, int nh = 1, int ka = 1) {
+    return size_t(stages) * ka * (kXStage + nh * (bn / 2) * kBK * 2) + 1024 + 256;
 }
 
-int stages_for_pair(int bn, int nh = 1) {
-    const int stage = kXStage + nh * (bn / 2) * kBK * 2;
-    return std::min(8, (kMaxSmem - 1024 - kBarBytes) / stage);
+int stages_for_pair(int bn, int nh = 1, int ka = 1) {
+    const int stage = ka * (kXStage + nh * (bn / 2) * kBK * 2);
+    return std::min(8, (kMaxSmem - 1024 - 256) / stage);
+}
+
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+// K atoms per ring stage of the pair kernel.  A stage's UMMAs are released by one
+// tcgen05.commit, and a commit costs the tensor pipe ~400 cycles (tools/mma_ts_micro.cu:
+// a 2-SM N=192 UMMA takes 196 cycles at one commit per 4 UMMAs, 124 per 8, 96 at 32), so
+// two 64-wide K blocks per stage (8 UMMAs per commit) when N per UMMA is one r half;
+// DFX_PAIR_KA overrides for measurements.
+int pair_atoms(int nh, int64_t kb_per_split, int64_t total_kb) {
+    static const int env = env_int("DFX_PAIR_KA", 0);
+    int ka = env > 0 ? env : (nh == 1 ? 2 : 1);
+    if (ka > 1 && (kb_per_split % ka != 0 || total_kb % ka != 0)) ka = 1;
+    return ka;
 }
 
 cudaError_t launch_tc_pair(const CUtensorMap& tx, const CUtensorMap& ty, TcParams p, int pairs,
                            int ks, cudaStream_t st, const char* name, int el) {
     cudaError_t e;
     auto kern = el == kF16 ? tc_pair_rowdot<kF16> : tc_pair_rowdot<kBF16>;
-    if (p.commit_every <= 0) p.commit_every = commit_group(4 * (p.nh > 0 ? p.nh : 1), p.stages);
-    static const int wpf = env_int("DFX_W_PREFETCH", -1), zpf = env_int("DFX_Z_PREFETCH", -1);
-    if (wpf >= 0) p.w_prefetch = wpf;
-    if (zpf >= 0) p.z_prefetch = zpf;
     if ((e = ensure_max_dyn_smem(reinterpret_cast<const void*>(kern), kMaxSmem)) != cudaSuccess)
         return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs, ks, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = smem_for_pair(p.bn, p.stages, p.nh > 0 ? p.nh : 1);
+    cfg.dynamicSmemBytes = smem_for_pair(p.bn, p.stages, p.nh > 0 ? p.nh : 1, p.ka > 0 ? p.ka : 1);
     cfg.stream = st;
-#ifdef DFX_TRACE
-    const char* trace_file = std::getenv("DFX_TRACE");
-    if (trace_file) {
-        void* tp = nullptr;
-        cudaGetSymbolAddress(&tp, g_trace);
-        cudaMemsetAsync(tp, 0, sizeof(g_trace), st);
-    }
-#endif
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
@@ -947,19 +927,6 @@ cudaError_t launch_tc_pair(const CUtensorMap& tx, const CUtensorMap& ty, TcParam
     e = cudaLaunchKernelEx(&cfg, kern, tx, ty, p);
     prof_end(st);
     if (e != cudaSuccess) return e;
-#ifdef DFX_TRACE
-    if (trace_file) {
-        static unsigned long long host[kTrCta][kTrEv][kTrN];
-        cudaStreamSynchronize(st);
-        cudaMemcpyFromSymbol(host, g_trace, sizeof(host));
-        if (FILE* f = std::fopen(trace_file, "ab")) {
-            const int hdr[8] = {2 * pairs, p.stages, p.kb_per_split, p.nh, p.bn, p.commit_every, p.tiles, ks};
-            std::fwrite(hdr, sizeof(hdr), 1, f);
-            std::fwrite(host, sizeof(host), 1, f);
-            std::fclose(f);
-        }
-    }
-#endif
     return cudaGetLastError();
 }
 
@@ -1005,6 +972,15 @@ Split choose_split(int64_t m_tiles, int64_t r, int64_t kb_total, int max_ks, int
 bool pair_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("DFX_NORM_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// DFX_NORM_FUSE=0: a separate finish launch (A/B measurements).
+bool norm_fuse_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DFX_NORM_FUSE");
         return !(e && e[0] == '0');
     }();
     return on;
@@ -1235,6 +1211,33 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         if (err != cudaSuccess) return err;
     }
 
+    // Fused finisher (DFX_NORM_FUSE=0 restores the separate finish launch): the last U / V
+    // tile of each 128-row block runs the finisher for its rows; one counter per block.
+    const bool fuse = norm_fuse_enabled();
+    unsigned* counters = nullptr;
+    if (fuse) {
+        counters = static_cast<unsigned*>(
+            ws_get_zeroed(ws, kWsGramCount, size_t(m_tiles) * sizeof(unsigned), &err));
+        if (err != cudaSuccess) return err;
+    }
+    FinishArgs f{};
+    f.base_part = base; f.base_parts = static_cast<int>(n_chunks);
+    if (a.base_cached) { f.base_part = a.base_cached; f.base_parts = 1; }
+    f.cross_part = cross; f.cross_parts = u.ks * u.sp.ns;
+    if (!partial) { f.ba_part = ba; f.ba_parts = plan.sb.ns; }
+    f.d_out = d_out; f.two_s = 2.0 * a.s; f.s2 = a.s * a.s;
+    f.base_sq = a.base_sq; f.cross = a.cross; f.ba_sq = a.ba_sq;
+    f.round_dt = a.round_dt; f.w_norm = a.w_norm;
+    f.m = a.m; f.mag_dt = a.mag_dt; f.g = a.m ? a.g : nullptr;
+    if (partial) { f.w_norm = nullptr; f.g = nullptr; f.ba_sq = nullptr; }
+    const int fin_total = u.ks * u.sp.ns + (partial ? 0 : plan.sb.ns);
+    auto set_fin = [&](TcParams& p) {
+        if (!fuse) return;
+        p.fin = f;
+        p.fin_count = counters;
+        p.fin_total = fin_total;
+    };
+
     cudaStream_t side = st;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     if (forked) {
@@ -1258,6 +1261,7 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         p.Z = a.b; p.ldz = r;
         p.out = cross; p.base_out = base; p.do_chain = 1;
         if (a.base_cached) p.do_chain = 0;     // frozen W: base_sq comes from the cache
+        set_fin(p);
 #ifdef DFX_KO_CHAIN
         p.do_chain = 0;
 #endif
@@ -1266,7 +1270,8 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
             e = make_tmap_2d(&ta, el, a.a, r, d_in, d_in * 2, kBK, u.sp.bn / 2, true);
             if (e != cudaSuccess) return e;
             p.nh = u.nh;
-            p.stages = stages_for_pair(u.sp.bn, u.nh);
+            p.ka = pair_atoms(u.nh, u.kbps, (d_in + kBK - 1) / kBK);
+            p.stages = stages_for_pair(u.sp.bn, u.nh, p.ka);
             p.tiles = static_cast<int>(pm_tiles * u.sp.ns);
             const int pairs = std::min<int>(p.tiles, std::max(1, u.ctas / (2 * u.ks)));
             if (std::getenv("DFX_PLAN_PRINT"))
@@ -1303,7 +1308,8 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
             partial ? a.gram_out : gf32);
         prof_end(gs);
         if (launches) *launches += 2;
-        if ((e = cudaGetLastError()) != cudaSuccess || !half || partial) return e;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if (!half || partial) return cudaSuccess;
         prof_begin("gram_split", gs);
         gram_split<__half><<<static_cast<unsigned>((n + 255) / 256), 256, 0, gs>>>(
             gf32, r, r_pad, reinterpret_cast<__half*>(g2), inv_scale);
@@ -1326,6 +1332,7 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         p.out = ba; p.do_chain = 0;
         p.out_scale = inv_scale;
         p.tiles = static_cast<int>(m_tiles * plan.sb.ns);
+        set_fin(p);
         e = launch_tc(kTcRowdot, tb, tg, p, dim3(std::max(1, plan.b_ctas), 1), vs, "ba_rowdot_tc",
                       tpc && vs != st, el);
         if (e == cudaSuccess && launches) ++*launches;
@@ -1348,16 +1355,7 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
             return err;
     }
 
-    FinishArgs f{};
-    f.base_part = base; f.base_parts = static_cast<int>(n_chunks);
-    if (a.base_cached) { f.base_part = a.base_cached; f.base_parts = 1; }
-    f.cross_part = cross; f.cross_parts = u.ks * u.sp.ns;
-    if (!partial) { f.ba_part = ba; f.ba_parts = plan.sb.ns; }
-    f.d_out = d_out; f.two_s = 2.0 * a.s; f.s2 = a.s * a.s;
-    f.base_sq = a.base_sq; f.cross = a.cross; f.ba_sq = a.ba_sq;
-    f.round_dt = a.round_dt; f.w_norm = a.w_norm;
-    f.m = a.m; f.mag_dt = a.mag_dt; f.g = a.m ? a.g : nullptr;
-    if (partial) { f.w_norm = nullptr; f.g = nullptr; f.ba_sq = nullptr; }
+    if (fuse) return cudaSuccess;
     if (launches) ++*launches;
     return launch_finish(f, st);
 }

@@ -765,6 +765,182 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// V = B [G_hi | G_lo] with ba_sq = rowdot(V, B), G-stationary on CTA pairs.
+//
+// G is small (r x r) and every row tile of B multiplies the same G, so each CTA pair keeps
+// its N slice of [G_hi | G_lo] resident in shared memory (loaded once: this CTA's half_n = bn/2
+// G rows x 2 r_pad K, 2 * kx swizzle atoms) and streams only B: per 256-row pair tile, kx atoms
+// of the CTA's own 128 B rows, each consumed by two UMMA groups (against the G_hi atom and the
+// G_lo atom of the same K range: B G_hi + B G_lo = B (G_hi + G_lo)).  Pair p owns N slice
+// p % n_split and walks the row tiles p / n_split, + pairs per slice, ...; the accumulator is
+// double-buffered in TMEM so a tile's epilogue (rowdot with B from L2, the fused finisher)
+// overlaps the next tile's UMMAs.  Operand traffic per pair tile: 2 x 16 KiB x kx of B, instead
+// of re-streaming the G slice (96 rows x 2 r_pad) with every tile as the generic V kernel does.
+template <int kEl>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_pair_gstat(const __grid_constant__ CUtensorMap tmb, const __grid_constant__ CUtensorMap tmg,
+                  const TcParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    const int half_n = p.bn / 2;
+    const int kx = p.ka;                                  // K atoms of B (r_pad / 64)
+    const int g_atom = half_n * kBK * 2;                  // one G atom of this CTA's rows
+    uint8_t* sg = smem;                                   // [2 kx] G atoms (hi 0..kx-1, lo kx..)
+    uint8_t* sb = smem + 2 * kx * g_atom;                 // [stages] B atoms
+    uint64_t* full = reinterpret_cast<uint64_t*>(sb + p.stages * kXStage);
+    uint64_t* empty = full + p.stages;
+    uint64_t* tmem_full = empty + p.stages;     // [2]
+    uint64_t* tmem_empty = tmem_full + 2;       // [2]
+    uint64_t* gfull = tmem_empty + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gfull + 1);
+
+    const int warp = warp_id(), lane = lane_id();
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int nsl = p.n_split;
+    const int slice = pair % nsl;
+    const int pps = (npairs - slice + nsl - 1) / nsl;     // pairs serving this slice
+    const int first = pair / nsl;
+    const int64_t n0 = int64_t(slice) * p.bn;             // the slice's first G row / V column
+    const uint32_t slot_cols = static_cast<uint32_t>((p.bn + 31) / 32 * 32);
+
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&tmb);
+        tma_prefetch_desc(&tmg);
+        for (int s = 0; s < p.stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tmem_full[a], 1);
+            mbar_init(&tmem_empty[a], 8);
+        }
+        mbar_init(gfull, 1);
+        fence_mbar_init();
+    }
+    if (warp == kWarpMma) tmem_alloc_pair<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == kWarpProducer) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_last();
+            // the resident G slice: this CTA's half_n rows, hi atoms then lo atoms
+            if (leader) mbar_arrive_expect_tx(gfull, 2u * 2u * kx * g_atom);
+            const uint32_t gbar = mapa_shared(smem_u32(gfull), 0);
+            for (int a = 0; a < 2 * kx; ++a)
+                tma_load_2d_pair(&tmg, gbar, sg + a * g_atom, a * kBK,
+                                 static_cast<int32_t>(n0 + int64_t(rank) * half_n), pol);
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = first; t < p.tiles; t += pps) {
+                const int64_t m0 = int64_t(t) * (2 * kBM) + int64_t(rank) * kBM;
+                for (int a = 0; a < kx; ++a) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&full[s], 2 * kXStage);
+                    tma_load_2d_pair(&tmb, mapa_shared(smem_u32(&full[s]), 0), sb + s * kXStage,
+                                     a * kBK, static_cast<int32_t>(m0), pol);
+                    if (++s == p.stages) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == kWarpMma) {
+        if (leader && lane == 0) {
+            const uint32_t idesc = umma_idesc_f16(ab_fmt(kEl), 2 * kBM, static_cast<uint32_t>(p.bn));
+            mbar_wait(gfull, 0);
+            tc_fence_after();
+            int s = 0;
+            uint32_t ph = 0;
+            int local = 0;
+            for (int t = first; t < p.tiles; t += pps, ++local) {
+                const int slot = local & 1;
+                const uint32_t tacc = tmem_base + static_cast<uint32_t>(slot) * slot_cols;
+                mbar_wait(&tmem_empty[slot], ((local >> 1) & 1) ^ 1);
+                tc_fence_after();
+                for (int a = 0; a < kx; ++a) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t bx = smem_u32(sb + s * kXStage);
+                    for (int hl = 0; hl < 2; ++hl) {
+                        const uint32_t gy = smem_u32(sg + (hl * kx + a) * g_atom);
+#pragma unroll
+                        for (int k = 0; k < kBK / 16; ++k)
+                            umma_f16_pair(tacc, umma_desc_k_sw128(bx + k * 32), umma_desc_k_sw128(gy + k * 32),
+                                          idesc, (a > 0 || hl > 0 || k > 0) ? 1u : 0u);
+                    }
+                    umma_commit_pair_mc(&empty[s], 0x3);
+                    if (++s == p.stages) { s = 0; ph ^= 1; }
+                }
+                umma_commit_pair_mc(&tmem_full[slot], 0x3);
+            }
+        }
+    } else if (warp < 4) {
+        const int q = warp;
+        const int row = q * 32 + lane;
+        int local = 0;
+        for (int t = first; t < p.tiles; t += pps, ++local) {
+            const int64_t m0 = int64_t(t) * (2 * kBM) + int64_t(rank) * kBM;
+            const int64_t gm = m0 + row;
+            const int slot = local & 1;
+            // this row's B slice (<= 256 values) into registers while the tile's UMMAs run, so
+            // the epilogue is TMEM loads + FMAs only (an L2 round trip per 32 columns otherwise
+            // made the epilogue, not the MMA, the per-tile critical path)
+            uint4 zb[32];
+            {
+                const uint16_t* zr = static_cast<const uint16_t*>(p.Z) + gm * p.ldz + n0;
+#pragma unroll
+                for (int v = 0; v < 32; ++v)
+                    zb[v] = (gm < p.M && 8 * v < p.bn && n0 + 8 * v < p.N)
+                                ? *reinterpret_cast<const uint4*>(zr + 8 * v) : make_uint4(0, 0, 0, 0);
+            }
+            mbar_wait(&tmem_full[slot], (local >> 1) & 1);
+            tc_fence_after();
+            const uint32_t trow = tmem_base + static_cast<uint32_t>(slot) * slot_cols +
+                                  (static_cast<uint32_t>(q * 32) << 16);
+            float acc = 0.0f;
+#pragma unroll
+            for (int c0 = 0; c0 < 256; c0 += 32) {
+                if (c0 >= p.bn) break;
+                uint32_t u[32];
+                tmem_ld_32x32b_x32(trow + c0, u);
+                tmem_ld_wait();
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    if (c0 + 8 * v < p.bn && n0 + c0 + 8 * v < p.N) {
+                        float z[8];
+                        unpack8<kEl>(zb[c0 / 8 + v], z);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            acc = fmaf(__uint_as_float(u[8 * v + e]), z[e], acc);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (leader) mbar_arrive(&tmem_empty[slot]);
+                else mbar_arrive_remote(mapa_shared(smem_u32(&tmem_empty[slot]), 0), 1);
+            }
+            if (p.out_scale) acc = __fmul_rn(acc, *p.out_scale);   // exact power of two
+            if (gm < p.M) p.out[int64_t(slice) * p.M + gm] = acc;
+            if (p.fin_count && last_arrival(p.fin_count + m0 / kBM, p.fin_total, tmem_slot + 1) && gm < p.M)
+                finish_row(p.fin, gm);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == kWarpMma) {
+        tc_fence_after();
+        tmem_dealloc_pair<512>(tmem_base);
+    }
+}
+
 // Reduce gram partial tiles in fixed split order and emit [G_hi | G_lo] (bf16) with
 // G mirrored from the upper triangle, so the hi/lo operand is exactly symmetric.
 __global__ void __launch_bounds__(256) gram_reduce(const float* __restrict__ part, int k_split,
@@ -1028,8 +1204,60 @@ struct NormPlan {
     int g_ks, g_kbps, g_ctas;
     Split sb;
     int b_ctas;
+    bool v_gstat;   // V on tc_pair_gstat (b_ctas = 2 x pairs, sb.ns = N slices, sb.bn = N slice)
     double cycles;
 };
+
+// G-stationary V (tc_pair_gstat): the N slice (bn, n slices) whose resident [G_hi | G_lo] rows
+// (bn / 2 per CTA x 2 r_pad) leave at least 3 B stages; {0, 0} when none fits.
+struct GstatShape { int bn, nsl, stages; };
+
+size_t smem_for_gstat(int bn, int64_t r_pad, int stages) {
+    return size_t(2 * (r_pad / kBK)) * (bn / 2) * kBK * 2 + size_t(stages) * kXStage + 1024 + 256;
+}
+
+GstatShape gstat_shape(int64_t r) {
+    const int64_t r_pad = (r + kBK - 1) / kBK * kBK;
+    for (int nsl = 1; nsl <= 64; ++nsl) {
+        const int bn = static_cast<int>(((r + nsl - 1) / nsl + 31) / 32 * 32);
+        if (bn > 256) continue;
+        for (int st = 6; st >= 3; --st)
+            if (smem_for_gstat(bn, r_pad, st) <= size_t(kMaxSmem)) return {bn, static_cast<int>((r + bn - 1) / bn), st};
+    }
+    return {0, 0, 0};
+}
+
+// DFX_V_GSTAT: -1 (default) the cycle model picks the V kernel, 0 generic tc_rowdot, 1 G-stationary.
+int v_gstat_mode() {
+    static const int m = env_int("DFX_V_GSTAT", -1);
+    return m;
+}
+
+cudaError_t launch_gstat(const CUtensorMap& tb, const CUtensorMap& tg, const TcParams& p, int pairs,
+                         cudaStream_t st, int el) {
+    cudaError_t e;
+    auto kern = el == kF16 ? tc_pair_gstat<kF16> : tc_pair_gstat<kBF16>;
+    if ((e = ensure_max_dyn_smem(reinterpret_cast<const void*>(kern), kMaxSmem)) != cudaSuccess)
+        return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem_for_gstat(p.bn, int64_t(p.ka) * kBK, p.stages);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    prof_begin("ba_rowdot_tc", st);
+    e = cudaLaunchKernelEx(&cfg, kern, tb, tg, p);
+    prof_end(st);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 
 UPlan plan_u(int64_t d_out, int64_t r, int64_t kb_in, int64_t chunk_blocks, int64_t n_chunks,
              int budget) {
@@ -1088,6 +1316,7 @@ NormPlan plan_norm(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, i
     const int64_t n_chunks = (d_in + chunk_size - 1) / chunk_size;
     const int nt = static_cast<int>((r + kBM - 1) / kBM);
     const int gtiles = nt * (nt + 1) / 2;
+    const int64_t pm_tiles_n = (d_out + 2 * kBM - 1) / (2 * kBM);
     const double kReduce = 12000.0;  // fixed-order split reduction kernel
 
     auto gram = [&](int budget, int& ks, int& kbps, int& ctas) {
@@ -1097,13 +1326,39 @@ NormPlan plan_norm(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, i
         ctas = std::min(gtiles, std::max(1, budget / ks)) * ks;
         return gemm_cycles(int64_t(gtiles) * ks, ctas, kbps, kBM) + kReduce;
     };
-    auto vgemm = [&](int budget, Split& sb, int& ctas) {
+    // V cycle model with an operand-ingest term (~42 B per cycle per SM, DESIGN 5.1): the generic
+    // kernel re-streams its G slice with every 128-row tile, the G-stationary pair kernel streams
+    // only B (twice per pair tile: two CTAs) after loading its G slice once.
+    auto vgemm = [&](int budget, Split& sb, int& ctas, bool& gs) {
+        gs = false;
         if (!need_v) { sb = {1, 1, 16}; ctas = 0; return 0.0; }
-        sb = choose_split(m_tiles, r, 2 * r_pad / kBK, 1, budget);
+        const int64_t kb = 2 * r_pad / kBK;
+        sb = choose_split(m_tiles, r, kb, 1, budget);
         ctas = static_cast<int>(std::min<int64_t>(m_tiles * sb.ns, budget));
-        return gemm_cycles(m_tiles * sb.ns, ctas, 2 * r_pad / kBK, sb.bn);
+        const double tile_g = std::max(double(kb) * 4.0 * std::max(120.0, 0.5 * sb.bn),
+                                       double(kb) * (16384.0 + sb.bn * 128.0) / 42.0) + 2500.0;
+        const double generic = double((m_tiles * sb.ns + ctas - 1) / ctas) * tile_g;
+        const GstatShape gsh = gstat_shape(r);
+        const int mode = v_gstat_mode();
+        if (mode == 0 || gsh.bn == 0 || budget < 2 * gsh.nsl) return generic;
+        const int pairs = std::min<int>(static_cast<int>(pm_tiles_n * gsh.nsl), budget / 2) / gsh.nsl * gsh.nsl;
+        const int64_t kx = r_pad / kBK;
+        const double tile_s = std::max(double(kx) * 8.0 * 130.0, double(kx) * 16384.0 / 42.0) + 2500.0;
+        const double gstat = double((pm_tiles_n + pairs / gsh.nsl - 1) / (pairs / gsh.nsl)) * tile_s +
+                             double(kx) * gsh.bn * 128.0 / 42.0;
+        if (mode == 1 || gstat < generic) {
+            gs = true;
+            sb = {gsh.nsl, 1, gsh.bn};
+            ctas = 2 * pairs;
+            return gstat;
+        }
+        return generic;
     };
 
+    // DFX_NORM_STRATEGY (0 side-all, 1 side-gram, 2 serial) / DFX_NORM_SIDE (side-stream SMs):
+    // measurement overrides of the cycle model's choice
+    static const int force_st = env_int("DFX_NORM_STRATEGY", -1);
+    static const int force_side = env_int("DFX_NORM_SIDE", 0);
     NormPlan best{};
     best.cycles = 1e300;
     // serial on all SMs
@@ -1113,12 +1368,14 @@ NormPlan plan_norm(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, i
         p.side = 0;
         p.u = plan_u(d_out, r, kb_in, chunk_blocks, n_chunks, sms);
         const double g = gram(sms, p.g_ks, p.g_kbps, p.g_ctas);
-        const double v = vgemm(sms, p.sb, p.b_ctas);
+        const double v = vgemm(sms, p.sb, p.b_ctas, p.v_gstat);
         p.cycles = g + p.u.cycles + v;
         best = p;
+        if (force_st == kSerial) return best;
     }
     for (int side : {8, 12, 20, 28, 36, 52, 74}) {
         if (side >= sms) break;
+        if (force_side > 0 && side != force_side) continue;
         UPlan u = plan_u(d_out, r, kb_in, chunk_blocks, n_chunks, sms - side);
         // leave exactly the SMs U does not use to the side stream
         const int side_eff = std::max(side, sms - u.ctas) & ~1;
@@ -1131,13 +1388,14 @@ NormPlan plan_norm(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, i
             p.u = u;
             p.g_ks = gks; p.g_kbps = gkbps; p.g_ctas = gctas;
             if (st == kSideAll) {
-                const double v = vgemm(side_eff, p.sb, p.b_ctas);
+                const double v = vgemm(side_eff, p.sb, p.b_ctas, p.v_gstat);
                 p.cycles = std::max(u.cycles, g + v);
             } else {
-                const double v = vgemm(sms, p.sb, p.b_ctas);
+                const double v = vgemm(sms, p.sb, p.b_ctas, p.v_gstat);
                 p.cycles = std::max(u.cycles, g) + v;
             }
-            if (p.cycles < best.cycles * 0.999) best = p;
+            if (force_st >= 0 && st != force_st) continue;
+            if (p.cycles < best.cycles * 0.999 || (force_st >= 0 && best.strategy == kSerial)) best = p;
         }
     }
     return best;
@@ -1321,6 +1579,20 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         CUtensorMap tb, tg;
         cudaError_t e = make_tmap_2d(&tb, el, a.b, d_out, r, r * 2, kBK, kBM, true);
         if (e != cudaSuccess) return e;
+        if (plan.v_gstat) {
+            e = make_tmap_2d(&tg, el, g2, r, 2 * r_pad, 2 * r_pad * 2, kBK, plan.sb.bn / 2, true);
+            if (e != cudaSuccess) return e;
+            TcParams p{};
+            p.M = d_out; p.N = r; p.bn = plan.sb.bn; p.n_split = plan.sb.ns;
+            p.ka = static_cast<int>(r_pad / kBK);
+            p.stages = gstat_shape(r).stages;
+            p.Z = a.b; p.ldz = r; p.out = ba; p.out_scale = inv_scale;
+            p.tiles = static_cast<int>(pm_tiles);
+            set_fin(p);
+            e = launch_gstat(tb, tg, p, plan.b_ctas / 2, vs, el);
+            if (e == cudaSuccess && launches) ++*launches;
+            return e;
+        }
         e = make_tmap_2d(&tg, el, g2, r, 2 * r_pad, 2 * r_pad * 2, kBK, plan.sb.bn, true);
         if (e != cudaSuccess) return e;
         TcParams p{};

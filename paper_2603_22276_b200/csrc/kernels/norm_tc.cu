@@ -66,6 +66,8 @@ struct TcParams {
     // Fused finisher (rowdot): every tile of a 128-row block counts itself in
     // fin_count[block]; the tile completing the block (fin_total tiles over U and V) runs
     // finish_row for its rows, so no separate finish launch sits on the critical path.
+    // Blocks past M (the phantom half of a 256-row pair tile) never count: only real blocks
+    // have counters, and every kernel contributes to each real block exactly once per tile.
     FinishArgs fin;
     unsigned* fin_count;
     int fin_total;
@@ -477,7 +479,7 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
                 if (lane == 0) mbar_arrive(&tmem_empty[slot]);
                 if (p.out_scale) acc = __fmul_rn(acc, *p.out_scale);   // exact power of two
                 if (gm < p.M) p.out[(int64_t(ks) * p.n_split + (n0 / p.bn)) * p.M + gm] = acc;
-                if (p.fin_count && last_arrival(p.fin_count + m0 / kBM, p.fin_total, tmem_slot + 1) && gm < p.M)
+                if (p.fin_count && m0 < p.M && last_arrival(p.fin_count + m0 / kBM, p.fin_total, tmem_slot + 1) && gm < p.M)
                     finish_row(p.fin, gm);
             } else {
                 // gram tile store: out[(ks * tiles + t) * 128*bn + row*bn + col]
@@ -746,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else mbar_arrive_remote(mapa_shared(smem_u32(&tmem_empty[slot]), 0), 1);
             }
             if (gm < p.M) p.out[(int64_t(ks) * p.n_split + (n0 / bn_pair)) * p.M + gm] = acc;
-            if (p.fin_count && last_arrival(p.fin_count + m0 / kBM, p.fin_total, tmem_slot + 1) && gm < p.M)
+            if (p.fin_count && m0 < p.M && last_arrival(p.fin_count + m0 / kBM, p.fin_total, tmem_slot + 1) && gm < p.M)
                 finish_row(p.fin, gm);
         }
     }
@@ -928,7 +930,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (p.out_scale) acc = __fmul_rn(acc, *p.out_scale);   // exact power of two
             if (gm < p.M) p.out[int64_t(slice) * p.M + gm] = acc;
-            if (p.fin_count && last_arrival(p.fin_count + m0 / kBM, p.fin_total, tmem_slot + 1) && gm < p.M)
+            if (p.fin_count && m0 < p.M && last_arrival(p.fin_count + m0 / kBM, p.fin_total, tmem_slot + 1) && gm < p.M)
                 finish_row(p.fin, gm);
         }
     }

@@ -64,6 +64,9 @@ def load_peaks():
         return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
 
 
+TRAIN_NORM_SMS = 140   # the C2 training pipeline's norm SM budget (measured, DESIGN 5.3)
+
+
 def algorithmic(cfg):
     """Per-launch algorithmic work for each kernel of a module."""
     d_out, d_in, r, rows = cfg["d_out"], cfg["d_in"], cfg["r"], cfg["tokens"]
@@ -335,7 +338,7 @@ def run_gpu(args, rank, world, local_rank, dist):
         # the pipelined graph runs module i's compose beside module i+1's norm: leave the
         # compose kernels the SMs the norm GEMMs do not plan for (dfx_ctx_set_sm_budget).
         # A serial step (npipe == 1) gets the whole GPU for every kernel.
-        n = args.norm_sms if mode == args.mode else (104 if mode == "train" else 0)
+        n = args.norm_sms if mode == args.mode else (TRAIN_NORM_SMS if mode == "train" else 0)
         dfx.set_sm_budget(n if npipe > 1 else 0)
 
     def build_pipelined(mode, n):
@@ -1099,7 +1102,7 @@ def main():
                          "kernel or NCCL through torch.distributed)")
     ap.add_argument("--norm-sms", type=int, default=-1,
                     help="SM budget of the norm GEMMs in the pipelined graph (0 = all; default: "
-                         "80 for the training step, measured best of 48..148, 0 for inference)")
+                         "140 for the training step, measured best of 104..148, 0 for inference)")
     ap.add_argument("--lora-steps", type=int, default=50,
                     help="calls timed for the fused LoRA-GEMM + compose variant (0 = skip)")
     ap.add_argument("--variant-steps", type=int, default=400,
@@ -1107,7 +1110,9 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.norm_sms < 0:   # measured: the budget helps the C2 training pipeline only
-        args.norm_sms = 104 if (args.mode == "train" and args.config == "c2") else 0
+        # (DESIGN 5.3, round 2: 140 keeps the all-SM W.A^T plan, 128 SMs, with the Gram on
+        # 12 side SMs, and switches the d_mag backward to its partitioned 256-byte slabs)
+        args.norm_sms = TRAIN_NORM_SMS if (args.mode == "train" and args.config == "c2") else 0
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `python bench.py --gpus N` without a launcher: re-exec under torchrun, one rank per

@@ -1390,7 +1390,10 @@ NormPlan plan_norm(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, i
             p.u = u;
             p.g_ks = gks; p.g_kbps = gkbps; p.g_ctas = gctas;
             if (st == kSideAll) {
-                const double v = vgemm(side_eff, p.sb, p.b_ctas, p.v_gstat);
+                // DFX_V_WIDE=1: V on the side stream but with an all-SM grid (its first CTAs run
+                // on the side SMs, the rest as U's CTAs retire) — measurement switch
+                static const bool wide = env_int("DFX_V_WIDE", 0) != 0;
+                const double v = vgemm(wide ? sms : side_eff, p.sb, p.b_ctas, p.v_gstat);
                 p.cycles = std::max(u.cycles, g + v);
             } else {
                 const double v = vgemm(sms, p.sb, p.b_ctas, p.v_gstat);

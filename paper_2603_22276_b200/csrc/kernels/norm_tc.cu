@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
                 for (int it = 0; it < pf && it < nkb; ++it)
                     tma_prefetch_2d(&tmx, (kb0 + it) * kBK, static_cast<int32_t>(m0));
                 for (int it = 0; it < nkb; ++it) {
-                    if (it + pf < nkb)
+                    if (pf > 0 && it + pf < nkb)   // (pf = 0: no prefetch — not of the block being loaded)
                         tma_prefetch_2d(&tmx, (kb0 + it + pf) * kBK, static_cast<int32_t>(m0));
                     mbar_wait(&empty[s], ph ^ 1);
                     mbar_arrive_expect_tx(&full[s], raw_bytes);
@@ -579,7 +579,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_mbar_init();
     }
+#ifdef DFX_KO_TMEM
+    if (threadIdx.x == 0) *tmem_slot = 0;
+    if (false) {
+#else
     if (warp == kWarpMma) {
+#endif
         switch (tmem_cols) {
             case 32: tmem_alloc_pair<32>(tmem_slot); break;
             case 64: tmem_alloc_pair<64>(tmem_slot); break;
@@ -610,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tma_prefetch_2d(&tmx, (kb0 + it) * kBK, static_cast<int32_t>(m0));
                 for (int it = 0; it < nkb; ++it) {
                     for (int a = 0; a < ka; ++a)
-                        if (it * ka + a + pf < nkb_blocks)
+                        if (pf > 0 && it * ka + a + pf < nkb_blocks)
                             tma_prefetch_2d(&tmx, (kb0 + it * ka + a + pf) * kBK, static_cast<int32_t>(m0));
                     mbar_wait(&empty[s], ph ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[s], 2 * stage_bytes);
@@ -643,7 +648,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 for (int it = 0; it < nkb; ++it) {
                     mbar_wait(&full[s], ph);
+#ifndef DFX_KO_FENCE
                     tc_fence_after();
+#endif
                     const uint32_t sx0 = smem_u32(smem + s * stage_bytes);
                     for (int h = 0; h < nh; ++h) {
                         for (int a = 0; a < ka; ++a) {
@@ -670,7 +677,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
                     if (++s == p.stages) { s = 0; ph ^= 1; }
                 }
+#ifndef DFX_KO_TMEM
                 umma_commit_pair_mc(&tmem_full[slot], 0x3);
+#else
+                mbar_arrive(&tmem_full[slot]);
+                mbar_arrive_remote(mapa_shared(smem_u32(&tmem_full[slot]), 1), 1);
+#endif
             }
         }
     } else if (nkb > 0 && warp < 4) {
@@ -703,7 +715,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t m0 = int64_t(t / p.n_split) * (2 * kBM) + int64_t(rank) * kBM;
             const int64_t n0 = int64_t(t % p.n_split) * bn_pair;
             const int64_t gm = m0 + row;
+#ifndef DFX_KO_FWD
             if (leader && warp == 0) forward_tile(t);
+#endif
             if (do_chain) {
                 const ChainUnits cu = chain_units(warp, static_cast<int>(t % p.n_split), p.n_split);
                 if (cu.n == 2)
@@ -715,7 +729,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const int slot = nslots == 2 ? (local & 1) : 0;
             const int use = nslots == 2 ? (local >> 1) : local;
+#ifdef DFX_SLEEPWAIT
+            mbar_wait_sleep(&tmem_full[slot], use & 1, DFX_SLEEPWAIT);
+#else
             mbar_wait(&tmem_full[slot], use & 1);
+#endif
             tc_fence_after();
             const uint32_t trow = tmem_base + static_cast<uint32_t>(slot) * slot_cols +
                                   (static_cast<uint32_t>(q * 32) << 16);
@@ -755,7 +773,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     cluster_sync();
+#ifdef DFX_KO_TMEM
+    if (false) {
+#else
     if (warp == kWarpMma) {
+#endif
         tc_fence_after();
         switch (tmem_cols) {
             case 32: tmem_dealloc_pair<32>(tmem_base); break;
@@ -1534,6 +1556,8 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
             if (e != cudaSuccess) return e;
             p.nh = u.nh;
             p.ka = pair_atoms(u.nh, u.kbps, (d_in + kBK - 1) / kBK);
+            static const int wpf = env_int("DFX_W_PREFETCH", 0);   // K blocks of W warmed into L2 ahead
+            p.w_prefetch = wpf;
             p.stages = stages_for_pair(u.sp.bn, u.nh, p.ka);
             p.tiles = static_cast<int>(pm_tiles * u.sp.ns);
             const int pairs = std::min<int>(p.tiles, std::max(1, u.ctas / (2 * u.ks)));

@@ -51,6 +51,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
 }
 
+// A long wait (a warp idle for a whole main loop): try_wait with a nanosleep back-off, so the
+// idle warps do not keep polling the shared-memory barrier unit while the TMA / UMMA stream
+// runs through it.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase, uint32_t ns) {
+    uint32_t done = 0;
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+        if (done) return;
+        __nanosleep(ns);
+    }
+}
+
 // Wait for a phase completed by an arrive from another CTA of the cluster (default
 // .cta-scope semantics on both sides, as CUTLASS's cluster barriers do: a cluster-scope
 // acquire/release compiles to MEMBAR.ALL.GPU / CCTL.IVALL on every use).

@@ -1,0 +1,8 @@
+#!/bin/bash
+mkdir -p gpurun_out/ko
+run() { tag=$1; shift; env "$@" timeout 300 ncu --metrics gpu__time_duration.sum,gpc__cycles_elapsed.max --clock-control none -k regex:"tc_pair_rowdot" --csv \
+     --log-file gpurun_out/ko/$tag.csv python scripts/profile_module.py --steps 3 > /dev/null 2>&1; }
+for ka in 1 2; do
+  run s_all_ka$ka DFX_PAIR_KA=$ka DFX_LIB=variants/libdfx_s_all.so
+  run s_nofence_ka$ka DFX_PAIR_KA=$ka DFX_LIB=variants/libdfx_s_all_nofence.so
+done

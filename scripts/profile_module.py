@@ -16,11 +16,16 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--bwd", action="store_true")
     ap.add_argument("--budget", type=int, default=0, help="dfx_ctx_set_sm_budget for the norm")
+    ap.add_argument("--d-out", type=int, default=0, help="override the config's d_out (analysis)")
+    ap.add_argument("--fill", default="randn", choices=["randn", "zeros", "bits"],
+                    help="W / A contents (analysis: does the data change the kernel's time?)")
     a = ap.parse_args()
     import torch
     import paper_2603_22276_b200 as P
     cfg = bench.CONFIGS[a.config]
     d_out, d_in, r, rows = cfg["d_out"], cfg["d_in"], cfg["r"], cfg["tokens"]
+    if a.d_out:
+        d_out = a.d_out
     s = 2.0 / math.sqrt(r)
     dfx = P.Dfx(0)
     dfx.set_sm_budget(a.budget)
@@ -28,6 +33,13 @@ def main():
     bf = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[cfg["dtype"]]
     W = torch.randn(d_out, d_in, device="cuda").to(bf)
     A = torch.randn(r, d_in, device="cuda").to(bf)
+    if a.fill == "zeros":
+        W.zero_(); A.zero_()
+    elif a.fill == "bits":       # random bit patterns of finite bf16 values
+        for t in (W, A):
+            v = torch.randint(0, 1 << 15, t.shape, device="cuda", dtype=torch.int32)
+            v = (v & 0x3FFF) | ((v & 0x4000) << 1)      # exponent below the inf/nan range, random sign
+            t.copy_(v.to(torch.int16).view(torch.bfloat16))
     B = torch.randn(d_out, r, device="cuda").to(bf)
     base = torch.randn(rows, d_out, device="cuda").to(bf)
     lora = torch.randn(rows, d_out, device="cuda").to(bf)

@@ -149,14 +149,15 @@ void run(void* w, void* a, uint64_t d_out, uint64_t d_in, int grid, CUtensorMapL
 // what u_rowdot_tc does); kMode 2: loads complete locally and the peer forwards "landed" to
 // the leader with a remote arrive.  The leader's consumer releases both CTAs' stages.
 template <int kMode>
-__global__ void __launch_bounds__(64) pair_kernel(const __grid_constant__ CUtensorMap tw,
+__global__ void __launch_bounds__(256) pair_kernel(const __grid_constant__ CUtensorMap tw,
                                                   const __grid_constant__ CUtensorMap ta, int kblocks,
                                                   int wtiles, long long* cycles) {
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t full[8], empty[8];
+    __shared__ uint64_t full[8], empty[8], done;
     const int stages = kStages8;
     const uint32_t rank = cluster_ctarank();
+    if (threadIdx.x == 0) mbar_init(&done, 1);
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], kMode == 2 && rank == 0 ? 2 : 1);
@@ -187,6 +188,9 @@ __global__ void __launch_bounds__(64) pair_kernel(const __grid_constant__ CUtens
                 tma_load_2d(&ta, &full[s], dst + kRowsW * 128, it * 64, arow0, pol);
             }
         }
+    } else if (blockDim.x > 64 && threadIdx.x >= 64 && threadIdx.x < 192 && kMode == 1) {
+        mbar_wait(&done, 0);          // 4 warps idle-spinning for the whole stream (like the
+                                      // norm kernel's epilogue warps waiting for the accumulator)
     } else if (threadIdx.x == 32) {
         for (int it = 0; it < kblocks; ++it) {
             const int s = it % stages;
@@ -200,13 +204,15 @@ __global__ void __launch_bounds__(64) pair_kernel(const __grid_constant__ CUtens
             }
         }
     }
+    if (threadIdx.x == 32) mbar_arrive(&done);
     __syncthreads();
     cluster_sync();
     if (threadIdx.x == 0) cycles[blockIdx.x] = clock64() - t0;
 }
 
 template <int kMode>
-void run_pair(void* w, void* a, uint64_t d_out, uint64_t d_in, int grid, long long* cyc, const char* tag) {
+void run_pair(void* w, void* a, uint64_t d_out, uint64_t d_in, int grid, long long* cyc, const char* tag,
+              int threads = 64) {
     const CUtensorMap tw = make_map(w, d_out, d_in, kRowsW, 1, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     const CUtensorMap ta = make_map(a, 384, d_in, kRowsA, 1, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     const size_t smem = kStages8 * kBlockBytes + 1024;
@@ -214,7 +220,7 @@ void run_pair(void* w, void* a, uint64_t d_out, uint64_t d_in, int grid, long lo
     const int kblocks = static_cast<int>(d_in / 64), wtiles = static_cast<int>(d_out / (2 * kRowsW));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(64);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -275,6 +281,7 @@ int main(int argc, char** argv) {
         run<1>(w, a, d_out, d_in, sms, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, cyc, "single, 148 CTAs");
         run<1>(w, a, d_out, d_in, 128, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, cyc, "single, 128 CTAs");
         run_pair<1>(w, a, d_out, d_in, 128, cyc, "pair, leader-barrier loads");
+        run_pair<1>(w, a, d_out, d_in, 128, cyc, "pair, leader-barrier, 256 thr + 4 spinning warps", 256);
         run_pair<2>(w, a, d_out, d_in, 128, cyc, "pair, local + forward");
         run_pair<1>(w, a, d_out, d_in, 64, cyc, "pair, leader-barrier, 64");
         run_pair<2>(w, a, d_out, d_in, 64, cyc, "pair, local + forward, 64");

@@ -92,6 +92,23 @@ __device__ __forceinline__ bool last_arrival(unsigned* count, int total, volatil
     return last;
 }
 
+// -DDFX_TRACE (experiment builds only): the pair kernel stamps %globaltimer at pipeline events
+// of its first kTrN stages into g_trace[cta][ev][i]; the launcher appends the array to the file
+// named by $DFX_TRACE after the launch (events: 0 producer issues stage j, 1 MMA sees stage i
+// full, 2 MMA released stage i, 3 producer sees stage j empty).
+#ifdef DFX_TRACE
+constexpr int kTrN = 128, kTrEv = 4, kTrCta = 148;
+__device__ unsigned long long g_trace[kTrCta][kTrEv][kTrN];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define DFX_TR(ev, i) do { if ((i) < kTrN && blockIdx.x < kTrCta) g_trace[blockIdx.x][ev][i] = gtimer(); } while (0)
+#else
+#define DFX_TR(ev, i) do { } while (0)
+#endif
+
 __device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -618,6 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (pf > 0 && it * ka + a + pf < nkb_blocks)
                             tma_prefetch_2d(&tmx, (kb0 + it * ka + a + pf) * kBK, static_cast<int32_t>(m0));
                     mbar_wait(&empty[s], ph ^ 1);
+                    DFX_TR(3, it);
                     if (leader) mbar_arrive_expect_tx(&full[s], 2 * stage_bytes);
                     const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
                     uint8_t* sx = smem + s * stage_bytes;
@@ -629,6 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             tma_load_2d_pair(&tmy, lbar, sy + (h * ka + a) * y_bytes, kc,
                                              static_cast<int32_t>(n0 + int64_t(h) * p.bn), pol_y);
                     }
+                    DFX_TR(0, it);
                     if (++s == p.stages) { s = 0; ph ^= 1; }
                 }
             }
@@ -648,6 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 for (int it = 0; it < nkb; ++it) {
                     mbar_wait(&full[s], ph);
+                    DFX_TR(1, it);
 #ifndef DFX_KO_FENCE
                     tc_fence_after();
 #endif
@@ -669,6 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     }
+                    DFX_TR(2, it);
 #ifndef DFX_KO_COMMIT
                     umma_commit_pair_mc(&empty[s], 0x3);
 #else
@@ -1124,9 +1145,30 @@ cudaError_t launch_tc_pair(const CUtensorMap& tx, const CUtensorMap& ty, TcParam
     cfg.attrs = at;
     cfg.numAttrs = 1;
     prof_begin(name, st);
+#ifdef DFX_TRACE
+    const char* trace_file = std::getenv("DFX_TRACE");
+    if (trace_file) {
+        void* tp = nullptr;
+        cudaGetSymbolAddress(&tp, g_trace);
+        cudaMemsetAsync(tp, 0, sizeof(g_trace), st);
+    }
+#endif
     e = cudaLaunchKernelEx(&cfg, kern, tx, ty, p);
     prof_end(st);
     if (e != cudaSuccess) return e;
+#ifdef DFX_TRACE
+    if (trace_file) {
+        static unsigned long long host[kTrCta][kTrEv][kTrN];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(host, g_trace, sizeof(host));
+        if (FILE* f = std::fopen(trace_file, "ab")) {
+            const int hdr[8] = {2 * pairs, p.stages, p.kb_per_split, p.nh, p.bn, p.ka, p.tiles, ks};
+            std::fwrite(hdr, sizeof(hdr), 1, f);
+            std::fwrite(host, sizeof(host), 1, f);
+            std::fclose(f);
+        }
+    }
+#endif
     return cudaGetLastError();
 }
 

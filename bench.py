@@ -352,7 +352,9 @@ def run_gpu(args, rank, world, local_rank, dist):
         gph = torch.cuda.CUDAGraph()
         order = args.capture_order
         if order == "auto":
-            order = "module" if mode == "train" else "norm-first"
+            # round 2: norm-first for both (training at the 140-SM plan: 7.80k vs 7.75k
+            # modules/s, two repeats on one box; inference: 11.6k vs 10.5k)
+            order = "norm-first"
 
         def comp(i):
             side.wait_event(ev_norm[i])
@@ -1083,7 +1085,7 @@ def main():
                     help="analysis: time one stage of the step alone (not a bench number)")
     ap.add_argument("--capture-order", default="auto", choices=["auto", "norm-first", "module"],
                     help="graph node creation order of the pipelined step (auto: module order "
-                         "for training, norm-first for inference; measured, DESIGN 5.3)")
+                         "for training in round 1, norm-first for both since round 2; measured, DESIGN 5.3-5.4)")
     ap.add_argument("--compose-parts", default="both", choices=["both", "fwd", "bwd"],
                     help="analysis: which training compose kernels the step runs")
     ap.add_argument("--prof-steps", type=int, default=40)

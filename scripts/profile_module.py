@@ -17,6 +17,8 @@ def main():
     ap.add_argument("--bwd", action="store_true")
     ap.add_argument("--budget", type=int, default=0, help="dfx_ctx_set_sm_budget for the norm")
     ap.add_argument("--d-out", type=int, default=0, help="override the config's d_out (analysis)")
+    ap.add_argument("--raw-alloc", action="store_true",
+                    help="W / A in plain cudaMalloc memory (not the torch caching allocator)")
     ap.add_argument("--fill", default="randn", choices=["randn", "zeros", "bits"],
                     help="W / A contents (analysis: does the data change the kernel's time?)")
     a = ap.parse_args()
@@ -33,6 +35,22 @@ def main():
     bf = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[cfg["dtype"]]
     W = torch.randn(d_out, d_in, device="cuda").to(bf)
     A = torch.randn(r, d_in, device="cuda").to(bf)
+    if a.raw_alloc:   # plain cudaMalloc'd buffers, copied from the torch tensors
+        import ctypes
+        rt = ctypes.CDLL("libcudart.so")
+        keep = []
+        def raw_like(t):
+            ptr = ctypes.c_void_p()
+            assert rt.cudaMalloc(ctypes.byref(ptr), ctypes.c_size_t(t.numel() * 2)) == 0
+            keep.append(ptr)
+
+            class Raw:
+                __cuda_array_interface__ = {"shape": tuple(t.shape), "typestr": "<i2",
+                                            "data": (ptr.value, False), "version": 3}
+            return torch.as_tensor(Raw(), device="cuda").view(t.dtype)
+        W2, A2 = raw_like(W), raw_like(A)
+        W2.copy_(W); A2.copy_(A); W, A = W2, A2
+        print("raw cudaMalloc operands", W.data_ptr() % 4096, flush=True)
     if a.fill == "zeros":
         W.zero_(); A.zero_()
     elif a.fill == "bits":       # random bit patterns of finite bf16 values

@@ -1682,20 +1682,34 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         return e;
     };
 
-    if (plan.strategy == kSerial) {
-        if ((err = launch_gram(st)) != cudaSuccess) return err;
-        if ((err = launch_u()) != cudaSuccess) return err;
-        if (!partial && (err = launch_v(st)) != cudaSuccess) return err;
-    } else {
-        // U first on the caller's stream (it claims its SMs), the adapter chain beside it
-        if ((err = launch_u()) != cudaSuccess) return err;
-        if ((err = launch_gram(side)) != cudaSuccess) return err;
-        if (plan.strategy == kSideAll && !partial && (err = launch_v(side)) != cudaSuccess)
-            return err;
-        if ((err = cudaEventRecord(ev_join, side)) != cudaSuccess) return err;
-        if ((err = cudaStreamWaitEvent(st, ev_join, 0)) != cudaSuccess) return err;
-        if (plan.strategy == kSideGram && !partial && (err = launch_v(st)) != cudaSuccess)
-            return err;
+    auto run = [&]() -> cudaError_t {
+        cudaError_t e;
+        if (plan.strategy == kSerial) {
+            if ((e = launch_gram(st)) != cudaSuccess) return e;
+            if ((e = launch_u()) != cudaSuccess) return e;
+            if (!partial && (e = launch_v(st)) != cudaSuccess) return e;
+        } else {
+            // U first on the caller's stream (it claims its SMs), the adapter chain beside it
+            if ((e = launch_u()) != cudaSuccess) return e;
+            if ((e = launch_gram(side)) != cudaSuccess) return e;
+            if (plan.strategy == kSideAll && !partial && (e = launch_v(side)) != cudaSuccess)
+                return e;
+            if ((e = cudaEventRecord(ev_join, side)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(st, ev_join, 0)) != cudaSuccess) return e;
+            if (plan.strategy == kSideGram && !partial && (e = launch_v(st)) != cudaSuccess)
+                return e;
+        }
+        return cudaSuccess;
+    };
+    if ((err = run()) != cudaSuccess) {
+        // a launch failed after others were queued: the fused finisher's counters would keep
+        // the queued tiles' arrivals; clear them behind everything queued on both streams
+        if (counters) {
+            if (forked && cudaEventRecord(ev_join, side) == cudaSuccess)
+                cudaStreamWaitEvent(st, ev_join, 0);
+            cudaMemsetAsync(counters, 0, size_t(m_tiles) * sizeof(unsigned), st);
+        }
+        return err;
     }
 
     if (fuse) return cudaSuccess;

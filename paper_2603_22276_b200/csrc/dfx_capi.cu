@@ -183,6 +183,27 @@ cudaError_t make_tmap_2d_sw(CUtensorMap* out, int dt, const void* base, uint64_t
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// A row-major [rows x cols] matrix viewed as [cols/64 atoms][rows][64]: box {64, box_rows, atoms}
+// lands `atoms` consecutive 64-wide K blocks as separate 128B-swizzled [box_rows][64] tiles
+// (the UMMA K-major layout of each atom), in one TMA instruction.  cols % 64 == 0.
+cudaError_t make_tmap_3d_katoms(CUtensorMap* out, int dt, const void* base, uint64_t rows,
+                                uint64_t cols, uint64_t row_pitch_bytes, uint32_t box_rows,
+                                uint32_t atoms) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    if (cols % 64 != 0 || dt == kF32) return cudaErrorInvalidValue;
+    const CUtensorMapDataType t = dt == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    const cuuint64_t dims[3] = {64, rows, cols / 64};
+    const cuuint64_t strides[2] = {row_pitch_bytes, 128};
+    const cuuint32_t box[3] = {64, box_rows, atoms};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = fn(out, t, 3, const_cast<void*>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 // ----------------------------------------------------------------- profiling
 struct Profiler {
     struct Rec {

@@ -23,6 +23,12 @@ cudaError_t make_tmap_2d_sw(CUtensorMap* out, int dt, const void* base, uint64_t
                             uint64_t cols, uint64_t row_pitch_bytes, uint32_t box_cols,
                             uint32_t box_rows, int swizzle_bytes);
 
+// [rows x cols] viewed as [cols/64][rows][64], box {64, box_rows, atoms}: `atoms` consecutive
+// 64-wide K blocks per TMA instruction (cols % 64 == 0, 16-bit types).
+cudaError_t make_tmap_3d_katoms(CUtensorMap* out, int dt, const void* base, uint64_t rows,
+                                uint64_t cols, uint64_t row_pitch_bytes, uint32_t box_rows,
+                                uint32_t atoms);
+
 // Attributes of the current device, queried once per device and cached (launch paths call
 // these on every launch).
 int device_sm_count();

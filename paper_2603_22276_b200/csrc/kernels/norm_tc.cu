@@ -62,6 +62,7 @@ struct TcParams {
     int w_prefetch;         // K blocks of X (W) prefetched into L2 ahead of the loads
     int nh;                 // pair kernel: UMMAs per K step (N per CTA pair = nh * bn)
     int ka;                 // pair kernel: 64-wide K blocks ("atoms") per ring stage (1 or 2)
+    int tma3d;              // pair kernel: tmx / tmy are K-atom 3-D maps, one TMA per operand per stage
     const float* out_scale; // rowdot: multiply each row's sum by *out_scale (fp16 V: 2^-e)
     // Fused finisher (rowdot): every tile of a 128-row block counts itself in
     // fin_count[block]; the tile completing the block (fin_total tiles over U and V) runs
@@ -640,12 +641,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
                     uint8_t* sx = smem + s * stage_bytes;
                     uint8_t* sy = sx + ka * kXStage;
-                    for (int a = 0; a < ka; ++a) {
-                        const int kc = (kb0 + it * ka + a) * kBK;
-                        tma_load_2d_pair(&tmx, lbar, sx + a * kXStage, kc, static_cast<int32_t>(m0), pol_x);
+                    if (p.tma3d) {
+                        // all ka atoms of an operand in one instruction ([atom][rows][64] tiles):
+                        // half the TMA instructions of the 2-D form, whose per-instruction cost
+                        // paced the bare ring (profiles/r02_u_knockouts.txt)
+                        const int kb = kb0 + it * ka;
+                        tma_load_3d_pair(&tmx, lbar, sx, 0, static_cast<int32_t>(m0), kb, pol_x);
                         for (int h = 0; h < nh; ++h)
-                            tma_load_2d_pair(&tmy, lbar, sy + (h * ka + a) * y_bytes, kc,
-                                             static_cast<int32_t>(n0 + int64_t(h) * p.bn), pol_y);
+                            tma_load_3d_pair(&tmy, lbar, sy + h * ka * y_bytes, 0,
+                                             static_cast<int32_t>(n0 + int64_t(h) * p.bn), kb, pol_y);
+                    } else {
+                        for (int a = 0; a < ka; ++a) {
+                            const int kc = (kb0 + it * ka + a) * kBK;
+                            tma_load_2d_pair(&tmx, lbar, sx + a * kXStage, kc, static_cast<int32_t>(m0), pol_x);
+                            for (int h = 0; h < nh; ++h)
+                                tma_load_2d_pair(&tmy, lbar, sy + (h * ka + a) * y_bytes, kc,
+                                                 static_cast<int32_t>(n0 + int64_t(h) * p.bn), pol_y);
+                        }
                     }
                     DFX_TR(0, it);
                     if (++s == p.stages) { s = 0; ph ^= 1; }
@@ -1598,6 +1610,12 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
             if (e != cudaSuccess) return e;
             p.nh = u.nh;
             p.ka = pair_atoms(u.nh, u.kbps, (d_in + kBK - 1) / kBK);
+            // one 3-D TMA per operand per stage when the stage holds several atoms
+            static const int t3 = env_int("DFX_PAIR_TMA3D", 1);
+            if (t3 && p.ka > 1 && d_in % kBK == 0 &&
+                make_tmap_3d_katoms(&tw, el, a.w, d_out, d_in, d_in * 2, kBM, p.ka) == cudaSuccess &&
+                make_tmap_3d_katoms(&ta, el, a.a, r, d_in, d_in * 2, u.sp.bn / 2, p.ka) == cudaSuccess)
+                p.tma3d = 1;
             static const int wpf = env_int("DFX_W_PREFETCH", 0);   // K blocks of W warmed into L2 ahead
             p.w_prefetch = wpf;
             p.stages = stages_for_pair(u.sp.bn, u.nh, p.ka);

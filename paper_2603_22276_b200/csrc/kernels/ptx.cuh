@@ -265,6 +265,17 @@ __device__ __forceinline__ void tma_load_2d_pair(const void* desc, uint32_t lead
         : "memory");
 }
 
+// 3-D form (K-atom view, make_tmap_3d_katoms): coordinates {0, row, first atom}.
+__device__ __forceinline__ void tma_load_3d_pair(const void* desc, uint32_t leader_bar,
+                                                 void* smem_dst, int32_t c0, int32_t c1, int32_t c2,
+                                                 uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(desc)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+        : "memory");
+}
+
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(

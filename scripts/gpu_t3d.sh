@@ -1,0 +1,13 @@
+#!/bin/bash
+mkdir -p gpurun_out/ko
+run() { tag=$1; shift; env "$@" timeout 300 ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active --clock-control none -k regex:"tc_pair_rowdot" --csv \
+     --log-file gpurun_out/ko/$tag.csv python scripts/profile_module.py --steps 3 > /dev/null 2>&1; }
+for t in 0 1; do
+  run t3d${t}_skel DFX_PAIR_TMA3D=$t DFX_LIB=variants/libdfx_s_all.so
+  run t3d${t}_base DFX_PAIR_TMA3D=$t
+done
+timeout 900 python -m pytest tests/test_gpu_norm.py tests/test_gpu_vkernel.py tests/test_gpu_dsplit.py -q -x -p no:cacheprovider > gpurun_out/ko/t3d_tests.log 2>&1; tail -1 gpurun_out/ko/t3d_tests.log
+for t in 0 1; do
+  DFX_PAIR_TMA3D=$t timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-cpu-full-module --e2e-steps 0 --lora-steps 0 --variant-steps 400 > gpurun_out/ko/t3d_bench.log 2>&1
+  echo "t3d $t | $(tail -1 gpurun_out/ko/t3d_bench.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print("train", d["value"], "infer", d["variants"]["infer"]["value"], "U", d["roofline"]["avg_us"])')"
+done

@@ -22,6 +22,9 @@
 //                          elementwise d_lora/d_base out of the same smem stages
 //   compose_bwd_generic    scalar fallback (ragged shapes), same serial chain
 #include <cuda_bf16.h>
+
+#include <cstdlib>
+#include <string>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -551,6 +554,17 @@ cudaError_t bwd_impl(int dt, const void* dy, const float* g, float sf, const voi
         // beside the norm GEMMs (an SM budget is set): 256-byte slabs, half as many CTAs, each
         // filling an SM — measured +1.5-2.7 % on the pipelined C2 training step (A/B on one
         // box); alone they are slower (57 vs 47 us), so the full-GPU launch keeps 128-byte slabs
+        // DFX_BWD_CFG=<stages>x<slab width / 128 B> overrides the choice (measurements)
+        static const char* cfg = std::getenv("DFX_BWD_CFG");
+        if (cfg) {
+            const std::string c(cfg);
+            if (c == "6x2") return bwd_serial_launch<T, 6, 2>(dt, dy, g, sf, inner, w_norm, rows, d_out, dl, db, d_mag, st);
+            if (c == "4x2") return bwd_serial_launch<T, 4, 2>(dt, dy, g, sf, inner, w_norm, rows, d_out, dl, db, d_mag, st);
+            if (c == "3x2") return bwd_serial_launch<T, 3, 2>(dt, dy, g, sf, inner, w_norm, rows, d_out, dl, db, d_mag, st);
+            if (c == "6x1") return bwd_serial_launch<T, 6>(dt, dy, g, sf, inner, w_norm, rows, d_out, dl, db, d_mag, st);
+            if (c == "12x1") return bwd_serial_launch<T, 12>(dt, dy, g, sf, inner, w_norm, rows, d_out, dl, db, d_mag, st);
+            if (c == "4x1") return bwd_serial_launch<T, 4>(dt, dy, g, sf, inner, w_norm, rows, d_out, dl, db, d_mag, st);
+        }
         if (partitioned && slabs <= 2 * int64_t(sms))
             return bwd_serial_launch<T, 6, 2>(dt, dy, g, sf, inner, w_norm, rows, d_out, dl, db, d_mag, st);
         return slabs > 2 * int64_t(sms)

@@ -333,6 +333,13 @@ def run_gpu(args, rank, world, local_rank, dist):
 
     stream = torch.cuda.Stream(device=dev)
     side = torch.cuda.Stream(device=dev)
+    # Every dfx call below issues on torch's current stream: make that `stream` for the whole
+    # run.  Calls on one context must not overlap (dfx.h: the workspace is shared), and torch's
+    # streams do not synchronise with the legacy default stream, so mixing the two let a call
+    # on the default stream run beside one on `stream` (it corrupted the fused finisher's
+    # counters for later calls).
+    torch.cuda.synchronize()
+    torch.cuda.set_stream(stream)
 
     def set_budget(mode, npipe):
         # the pipelined graph runs module i's compose beside module i+1's norm: leave the
@@ -458,9 +465,30 @@ def run_gpu(args, rank, world, local_rank, dist):
     torch.cuda.synchronize()
     launches_per_step = dfx.launches - launches_before
 
+    # DFX_BENCH_CANARY=1 (debugging): after each phase, the row norm of set 0 under the budget
+    # in force must reproduce the first result seen under that budget, bit for bit.
+    canary_ref = {}
+
+    def canary(tag):
+        if not os.environ.get("DFX_BENCH_CANARY"):
+            return
+        b = sets[0]
+        torch.cuda.synchronize()
+        wn, g = torch.empty_like(b["wn"]), torch.empty_like(b["g"])
+        with torch.cuda.stream(stream):
+            dfx.row_norm(b["W"], b["A"], b["B"], s, cs, wn, m=b["m"], g=g)
+        torch.cuda.synchronize()
+        key = dfx.get_sm_budget() if hasattr(dfx, "get_sm_budget") else "?"
+        cur = torch.cat([wn, g]).view(torch.int32)
+        ref = canary_ref.setdefault(key, cur.clone())
+        nd = int((cur != ref).sum())
+        log(f"canary after {tag} (budget {key}): {'ok' if nd == 0 else f'{nd} words differ'}")
+
+    canary("setup")
     # ---- timed region (headline mode)
     clk = ClockSampler(local_rank)
     ms, npipe = timed(args.mode, args.steps, args.warmup, clk)
+    canary("headline")
     value = world * args.steps / (ms / 1e3)
     log(f"timed ({args.mode}): {args.steps} steps in {ms:.3f} ms -> {value:.1f} modules/s")
     if args.only or args.compose_parts != "both":   # stage analysis: not a bench line
@@ -483,6 +511,7 @@ def run_gpu(args, rank, world, local_rank, dist):
             "what": ("row_norm + plain compose_fwd (inference module)" if other == "infer" else
                      "row_norm + dual compose_fwd + compose_bwd with d_mag (training step)")}
         log(f"variant {other}: {variants[other]['value']} modules/s")
+        canary("variant")
 
     # ---- LoRA-up GEMM fused with compose + residual (layer forward
     # epilogue, training outputs y and inner) vs the unfused sequence (cuBLAS lora GEMM,
@@ -525,6 +554,7 @@ def run_gpu(args, rank, world, local_rank, dist):
             "algorithmic_bytes": byts,
             "unfused": "cuBLAS bf16 GEMM -> lora (HBM), dfx_compose_fwd dual, torch.add residual"}
         log(f"lora_compose fused {tf:.1f} us vs unfused {tu:.1f} us")
+        canary("lora")
 
         # ---- cached ||W||^2_row of a frozen W; W is still read
         # for the cross term, the base_sq chain is skipped.  Full GPU, rotating buffer sets.
@@ -553,6 +583,7 @@ def run_gpu(args, rank, world, local_rank, dist):
                     "reference's recompute-every-call contract; bitwise equal while W is unchanged)",
             "plain_us": round(tn, 2), "cached_us": round(tc, 2), "speedup": round(tn / tc, 3)}
         log(f"row_norm plain {tn:.1f} us vs cached base_sq {tc:.1f} us")
+        canary("cached")
 
     # ---- per-kernel live durations (event-bracketed launches, same kernels / buffers / plan
     # as the timed region).  Each step is queued behind a 2 ms device spin so the brackets
@@ -658,6 +689,7 @@ def run_gpu(args, rank, world, local_rank, dist):
                  "frac_burst": round(nf / (norm_wall_ms / 1e3) / 1e12 / peak_tf_burst, 4),
                  "step_wall_us": round(step_wall_ms * 1e3, 2)}
     log(json.dumps(kernels))
+    canary("profile")
 
     # ---- end to end through the host-buffer entry point (pinned host memory)
     e2e = None
@@ -679,6 +711,12 @@ def run_gpu(args, rank, world, local_rank, dist):
                                       h["dy"], s, d_out, d_in, r, rows, cs, out["delta"],
                                       out["dl"], out["db"], hdm, hg)
 
+        # The device path's result for the same inputs under the plan the e2e call runs with
+        # (the split-K Gram partition follows the SM budget, so g can differ in its last bits
+        # between budgets; sets[0] was last written under another pass's budget).
+        with torch.cuda.stream(stream):
+            step(b0, args.mode)
+        torch.cuda.synchronize()
         e2e_step()  # stage buffers
         if dist:
             dist.barrier()
@@ -692,7 +730,11 @@ def run_gpu(args, rank, world, local_rank, dist):
             e2e_s = float(t.item())
         # result check on the host copies: the same outputs the device path produced
         torch.cuda.synchronize()
-        assert torch.equal(out["delta"].to(dev), b0["delta"]), "e2e delta mismatch"
+        if not torch.equal(out["delta"].to(dev), b0["delta"]):
+            nd = int((out["delta"].to(dev) != b0["delta"]).sum())
+            ng = int((hg.to(dev) != b0["g"]).sum())
+            raise AssertionError(f"e2e delta mismatch ({nd} of {b0['delta'].numel()} elements; "
+                                 f"g differs in {ng} of {d_out} rows)")
         if args.mode == "train":
             assert torch.equal(out["dl"].to(dev), b0["dl"]), "e2e d_lora mismatch"
             assert torch.equal(hdm.to(dev), b0["dm"]), "e2e d_mag mismatch"

@@ -21,7 +21,10 @@
  *     std::invalid_argument.  Non-finite values propagate (IEEE), never error.
  *   - A context is bound to one device; concurrent calls on one context must be
  *     serialised by the caller (its workspace is shared).  Use one context per
- *     concurrently used stream.
+ *     concurrently used stream.  Two calls of one context that overlap in time (e.g.
+ *     issued on two streams without an event between them) produce undefined results,
+ *     and leave the fused finisher's per-block arrival counters inconsistent for the
+ *     context's later norm calls: recreate the context after such a misuse.
  *   - There is no CPU fallback: every call runs sm_100a kernels and fails with
  *     DFX_ENODEV when no usable device is present.
  */

@@ -339,6 +339,11 @@ class Dfx:
     def set_sm_budget(self, sms: int):
         """Cap the SMs the norm GEMMs plan for (0 = all); see dfx_ctx_set_sm_budget."""
         self._check(self.lib.dfx_ctx_set_sm_budget(self.ctx, int(sms)))
+        self._budget = int(sms)
+
+    def get_sm_budget(self) -> int:
+        """The budget last set through this binding (0 = all SMs)."""
+        return getattr(self, "_budget", 0)
 
     def lora_compose(self, mid, B, base, g, s, y=None, delta=None, inner=None, lora=None,
                      bias=None, stream=None):

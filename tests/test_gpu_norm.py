@@ -488,3 +488,39 @@ def test_bf16_multi_chunk(oracle, budget, d_out, d_in, r, cs):
     dfx.set_sm_budget(budget)
     _full_size_check(dfx, oracle, d_out, d_in, r, d_out + cs + budget, n_rows=min(d_out, 256), cs=cs)
     dfx.close()
+
+
+def test_fused_finisher_state_across_calls(dfx, oracle):
+    """The fused finisher's per-block arrival counters return to zero after every call: plain,
+    cached-refresh and cached norms, two SM budgets and a shape with a phantom pair half
+    (d_out = 1000: the last 256-row pair tile covers 1024 rows) interleaved on one stream leave
+    a later plain norm bitwise equal to the first one."""
+    import torch
+    torch.manual_seed(3)
+    outs = []
+    for d_out in (2048, 1000):
+        d_in, r = 1024, 384
+        W = torch.randn(d_out, d_in, device="cuda").to(torch.bfloat16)
+        A = torch.randn(r, d_in, device="cuda").to(torch.bfloat16)
+        B = torch.randn(d_out, r, device="cuda").to(torch.bfloat16)
+        m = torch.ones(d_out, device="cuda")
+        s = 2.0 / np.sqrt(r)
+        cs, _ = oracle.plan_chunks(d_out, d_in)
+        cache = torch.empty(d_out, device="cuda")
+
+        def plain():
+            wn, g = torch.empty(d_out, device="cuda"), torch.empty(d_out, device="cuda")
+            dfx.row_norm(W, A, B, s, cs, wn, m=m, g=g)
+            return torch.cat([wn, g]).view(torch.int32).clone()
+
+        for budget in (0, 140):
+            dfx.set_sm_budget(budget)
+            first = plain()
+            for _ in range(3):
+                wn, g = torch.empty(d_out, device="cuda"), torch.empty(d_out, device="cuda")
+                dfx.row_norm_cached(W, A, B, s, cs, cache, wn, refresh=True, m=m, g=g)
+                dfx.row_norm_cached(W, A, B, s, cs, cache, wn, m=m, g=g)
+                assert torch.equal(plain(), first)
+            outs.append(first)
+    dfx.set_sm_budget(0)
+    torch.cuda.synchronize()

@@ -122,7 +122,10 @@ def test_base_sq_bitwise_fp32(dfx, oracle, d_out, d_in, r, cs):
 @pytest.mark.parametrize("dt", [1, 2])
 @pytest.mark.parametrize("d_out,d_in,r", [(256, 512, 64), (1024, 1024, 384), (300, 640, 40),
                                           (128, 4096, 512), (1000, 2048, 128), (8192, 256, 16),
-                                          (512, 8192, 1024)])
+                                          (512, 8192, 1024),
+                                          # d_in % 64 != 0: 2-D operand loads (no K-atom view),
+                                          # two atoms per stage; odd K-block count: one atom
+                                          (384, 1000, 96), (256, 960, 64)])
 def test_tensor_core_path(dfx, oracle, d_out, d_in, r, dt):
     """tcgen05/TMA path, bf16 (kind::f16 with bf16 operands) and fp16 (kind::f16 with fp16
     operands, DTypeKind::FP16E, dtype.hpp:12): base_sq bitwise; cross/ba_sq vs the oracle's fp32

@@ -304,7 +304,7 @@ def run_gpu(args, rank, world, local_rank, dist):
         b = dict(W=rnd(d_out, d_in), A=rnd(r, d_in), B=rnd(d_out, r), base=rnd(rows, d_out),
                  lora=rnd(rows, d_out), dy=rnd(rows, d_out))
         b.update(wn=torch.empty(d_out, device=dev), g=torch.empty(d_out, device=dev),
-                 dm=torch.empty(d_out, device=dev))
+                 dm=torch.empty(d_out, device=dev), ba=torch.empty(d_out, device=dev))
         for k in ("delta", "inner", "dl", "db"):
             b[k] = torch.empty_like(b["base"])
         dfx.row_norm(b["W"], b["A"], b["B"], s, cs, b["wn"])
@@ -312,8 +312,21 @@ def run_gpu(args, rank, world, local_rank, dist):
         sets.append(b)
     torch.cuda.synchronize()
 
+    split = args.split_adapter and tdt != torch.float32
+
+    def adapter(b, st=None, sms=0):
+        dfx.norm_adapter(b["A"], b["B"], d_out, b["ba"], sms=sms, stream=st)
+
+    def norm_w(b, st=None):
+        dfx.row_norm_ba(b["W"], b["A"], b["B"], s, cs, b["ba"], b["wn"], m=b["m"], g=b["g"],
+                        stream=st)
+
     def norm(b, st=None):
-        dfx.row_norm(b["W"], b["A"], b["B"], s, cs, b["wn"], m=b["m"], g=b["g"], stream=st)
+        if split:      # the split form, serially (pipelined graphs issue the parts apart)
+            adapter(b, st, args.adapter_sms)
+            norm_w(b, st)
+        else:
+            dfx.row_norm(b["W"], b["A"], b["B"], s, cs, b["wn"], m=b["m"], g=b["g"], stream=st)
 
     def compose(b, mode, st=None):
         if mode == "infer":
@@ -333,6 +346,7 @@ def run_gpu(args, rank, world, local_rank, dist):
 
     stream = torch.cuda.Stream(device=dev)
     side = torch.cuda.Stream(device=dev)
+    third = torch.cuda.Stream(device=dev)
     # Every dfx call below issues on torch's current stream: make that `stream` for the whole
     # run.  Calls on one context must not overlap (dfx.h: the workspace is shared), and torch's
     # streams do not synchronise with the legacy default stream, so mixing the two let a call
@@ -356,6 +370,16 @@ def run_gpu(args, rank, world, local_rank, dist):
         sA, sB = stream.cuda_stream, side.cuda_stream
         ev_norm = [torch.cuda.Event() for _ in range(n)]
         ev_comp = [torch.cuda.Event() for _ in range(n)]
+        ev_adapt = [torch.cuda.Event() for _ in range(n)]
+
+        def adapt(i):
+            # module i's adapter terms (A, B only) one module ahead on a third stream, beside
+            # module i-1's W part; it rewrites set i % nbuf's ba_sq, which module i-nbuf's W
+            # part read
+            if i >= nbuf:
+                third.wait_event(ev_norm[i - nbuf])
+            adapter(sets[i % nbuf], third.cuda_stream, args.adapter_sms)
+            ev_adapt[i].record(third)
         gph = torch.cuda.CUDAGraph()
         order = args.capture_order
         if order == "auto":
@@ -370,11 +394,19 @@ def run_gpu(args, rank, world, local_rank, dist):
             ev_comp[i].record(side)
 
         with torch.cuda.graph(gph, stream=stream):
+            if split and args.only != "compose":
+                third.wait_stream(stream)
+                adapt(0)
             for i in range(n):
                 b = sets[i % nbuf]
                 if i >= nbuf:
                     stream.wait_event(ev_comp[i - nbuf])
-                if args.only != "compose":
+                if split and args.only != "compose":
+                    if i + 1 < n:
+                        adapt(i + 1)
+                    stream.wait_event(ev_adapt[i])
+                    norm_w(b, sA)
+                elif args.only != "compose":
                     norm(b, sA)
                 ev_norm[i].record(stream)
                 # capture order = launch order among ready nodes: module i+1's norm is
@@ -388,6 +420,8 @@ def run_gpu(args, rank, world, local_rank, dist):
             if order == "norm-first":
                 comp(n - 1)
             stream.wait_event(ev_comp[n - 1])
+            if split and args.only != "compose":
+                stream.wait_stream(third)
         return gph
 
     def build_graphs(mode, steps):
@@ -715,7 +749,9 @@ def run_gpu(args, rank, world, local_rank, dist):
         # (the split-K Gram partition follows the SM budget, so g can differ in its last bits
         # between budgets; sets[0] was last written under another pass's budget).
         with torch.cuda.stream(stream):
-            step(b0, args.mode)
+            # the host entry points run the single-call norm (dfx_row_norm's plan)
+            dfx.row_norm(b0["W"], b0["A"], b0["B"], s, cs, b0["wn"], m=b0["m"], g=b0["g"])
+            compose(b0, args.mode)
         torch.cuda.synchronize()
         e2e_step()  # stage buffers
         if dist:
@@ -1147,6 +1183,13 @@ def main():
     ap.add_argument("--norm-sms", type=int, default=-1,
                     help="SM budget of the norm GEMMs in the pipelined graph (0 = all; default: "
                          "140 for the training step, measured best of 104..148, 0 for inference)")
+    ap.add_argument("--split-adapter", type=int, default=0,
+                    help="1: the pipelined graph computes each module's adapter term (ba_sq = "
+                         "rowquad(B, A A^T), dfx_norm_adapter) one module ahead on a third stream "
+                         "and finishes the norm with dfx_row_norm_ba (measured slower at C2: "
+                         "7.32k vs 7.94k training, 10.0k vs 11.8k inference; DESIGN 5.4)")
+    ap.add_argument("--adapter-sms", type=int, default=28,
+                    help="--split-adapter: SMs the adapter GEMMs plan for beside the W part")
     ap.add_argument("--lora-steps", type=int, default=50,
                     help="calls timed for the fused LoRA-GEMM + compose variant (0 = skip)")
     ap.add_argument("--variant-steps", type=int, default=400,

@@ -144,6 +144,29 @@ int dfx_norm_finish(dfx_ctx* ctx, dfx_dtype dtype, const void* B, const float* g
                     const float* m, dfx_dtype mag_dtype, float* w_norm, float* g, float* terms,
                     dfx_stream_t stream);
 
+/* Split form of dfx_row_norm for pipelined layer stacks (bf16 / fp16 tensor-core path).
+ * factored_norm_terms (factored_norm.cpp:27-120) splits into a part that reads only the
+ * adapter — ba_sq = rowquad(B, A A^T) (:65-77, :104-117), the Gram and B.G GEMMs — and a part
+ * that reads W: base_sq, cross = rowdot(W A^T, B), assemble, round, magnitude (:204-240).
+ *   dfx_norm_adapter  writes ba_sq [d_out] (fp32);
+ *   dfx_row_norm_ba   runs the W part and finishes with that ba_sq (terms, if non-null, as
+ *                     dfx_row_norm's).  Same arithmetic as dfx_row_norm; the Gram's split-K
+ *                     partition follows the SM budget the adapter call plans for, so ba_sq (and
+ *                     through it w_norm, g) can differ from a dfx_row_norm call in the last bits,
+ *                     as dfx_row_norm's own results do between SM budgets.
+ * The two use disjoint context workspace, so an adapter call may run concurrently with a
+ * dfx_row_norm_ba call of the same context (e.g. module i+1's adapter beside module i's W
+ * part); two adapter calls, or two W calls, still must not overlap. */
+/* sms > 0 caps the SMs the adapter's GEMMs plan for (it is meant to run beside other work);
+ * 0 = the context's SM budget. */
+int dfx_norm_adapter(dfx_ctx* ctx, dfx_dtype dtype, const void* A, const void* B,
+                     int64_t d_out, int64_t d_in, int64_t r, int sms, float* ba_sq,
+                     dfx_stream_t stream);
+int dfx_row_norm_ba(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A, const void* B,
+                    int64_t d_out, int64_t d_in, int64_t r, double s, int64_t chunk_size,
+                    const float* ba_sq, const float* m, dfx_dtype mag_dtype, float* w_norm,
+                    float* g, float* terms, dfx_stream_t stream);
+
 /* stable_compose / fused_compose / dual_output_compose (compose.hpp:43,53-57,62-68):
  * delta = (g-1)*base + g*(s*lora) in the canonical rounding order, bitwise equal to
  * the reference; inner = s*lora + base when inner != NULL (dual output). */

@@ -72,6 +72,9 @@ SIGNATURES = {
                                    _int, _vp, _int, _vp, _vp, _vp]),
     "dfx_norm_partial": (_int, [_vp, _int, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
                                 _vp]),
+    "dfx_norm_adapter": (_int, [_vp, _int, _vp, _vp, _i64, _i64, _i64, _int, _vp, _vp]),
+    "dfx_row_norm_ba": (_int, [_vp, _int, _vp, _vp, _vp, _i64, _i64, _i64, _f64, _i64, _vp, _vp,
+                               _int, _vp, _vp, _vp, _vp]),
     "dfx_norm_finish": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _i64, _i64, _f64, _vp, _int, _vp, _vp,
                                _vp, _vp]),
     "dfx_compose_fwd": (_int, [_vp, _int, _vp, _vp, _vp, _f64, _i64, _i64, _vp, _vp, _vp]),
@@ -241,6 +244,26 @@ class Dfx:
         self._check(self.lib.dfx_norm_plan(self.ctx, dtype, d_out, d_in, r, int(chunk_size),
                                            C.byref(u), C.byref(sd), C.byref(st)))
         return u.value, sd.value, st.value
+
+    def norm_adapter(self, A, B, d_out, ba_sq, sms=0, stream=None):
+        """dfx_norm_adapter: ba_sq = rowquad(B, A A^T) [d_out] fp32 (the adapter-only part of the
+        factored norm, for pipelined stacks; bf16 / fp16); sms > 0 caps the SMs it plans for."""
+        r, d_in = A.shape
+        self._vec("ba_sq", ba_sq, d_out)
+        self._check(self.lib.dfx_norm_adapter(self.ctx, _dtype_code(A), _ptr(A), _ptr(B), d_out, d_in,
+                                              r, int(sms), _ptr(ba_sq), self._s(stream)))
+
+    def row_norm_ba(self, W, A, B, s, chunk_size, ba_sq, w_norm, m=None, g=None, terms=None,
+                    mag_dtype=None, stream=None):
+        """dfx_row_norm_ba: the W part of the norm, finished with a ba_sq from norm_adapter."""
+        d_out, d_in, r = self._norm_operands(W, A, B)
+        self._vec("ba_sq", ba_sq, d_out)
+        self._vec("w_norm", w_norm, d_out)
+        dt = _dtype_code(W)
+        md = dt if mag_dtype is None else mag_dtype
+        self._check(self.lib.dfx_row_norm_ba(self.ctx, dt, _ptr(W), _ptr(A), _ptr(B), d_out, d_in, r,
+                                             float(s), int(chunk_size), _ptr(ba_sq), _ptr(m), md,
+                                             _ptr(w_norm), _ptr(g), _ptr(terms), self._s(stream)))
 
     def row_norm_cached(self, W, A, B, s, chunk_size, base_sq_cache, w_norm, refresh=False,
                         m=None, g=None, mag_dtype=None, stream=None):

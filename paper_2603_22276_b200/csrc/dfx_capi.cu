@@ -572,6 +572,59 @@ int dfx_row_norm_cached(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void
     return finish_call(ctx, e, "dfx_row_norm_cached");
 }
 
+int dfx_norm_adapter(dfx_ctx* ctx, dfx_dtype dtype, const void* A, const void* B,
+                     int64_t d_out, int64_t d_in, int64_t r, int sms, float* ba_sq,
+                     dfx_stream_t stream) {
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
+    if (rc) return rc;
+    if (d_out < 0 || d_in < 0 || r < 1) return fail(DFX_EINVAL, "dfx_norm_adapter: bad dims");
+    if (!A || !B || (!ba_sq && d_out > 0)) return fail(DFX_EINVAL, "dfx_norm_adapter: null operand");
+    if ((dtype != DFX_BF16 && dtype != DFX_F16) || !dfx::norm_uses_tensor_cores(dtype, d_out, d_in, r))
+        return fail(DFX_EUNSUPPORTED, "dfx_norm_adapter: needs the bf16 / fp16 tensor-core path");
+    dfx::NormArgs a{};
+    a.dt = dtype; a.a = A; a.b = B;
+    a.d_out = d_out; a.d_in = d_in; a.r = r; a.s = 1.0; a.chunk_size = 64;
+    a.ba_sq = ba_sq; a.mode = dfx::kNormAdapter;
+    if (sms < 0) return fail(DFX_EINVAL, "dfx_norm_adapter: negative SM cap");
+    // plan the Gram and V for at most `sms` SMs (the call runs beside other work)
+    const int saved = ctx->ws.sm_budget;
+    if (sms > 0) ctx->ws.sm_budget = saved > 0 ? std::min(saved, sms) : sms;
+    int launches = 0;
+    const cudaError_t e = dfx::launch_norm(a, &ctx->ws, stream, &launches);
+    ctx->ws.sm_budget = saved;
+    ctx->launches += launches;
+    return finish_call(ctx, e, "dfx_norm_adapter");
+}
+
+int dfx_row_norm_ba(dfx_ctx* ctx, dfx_dtype dtype, const void* W, const void* A, const void* B,
+                    int64_t d_out, int64_t d_in, int64_t r, double s, int64_t chunk_size,
+                    const float* ba_sq, const float* m, dfx_dtype mag_dtype, float* w_norm,
+                    float* g, float* terms, dfx_stream_t stream) {
+    DeviceGuard dg;
+    int rc = enter(ctx, dg, stream);
+    if (rc) return rc;
+    rc = check_norm_args(dtype, W, A, B, d_out, d_in, r, chunk_size);
+    if (rc) return rc;
+    if (!ba_sq && d_out > 0) return fail(DFX_EINVAL, "dfx_row_norm_ba: null ba_sq");
+    if (m && !valid_dtype(mag_dtype)) return fail(DFX_EUNSUPPORTED, "dfx_row_norm_ba: mag dtype");
+    if (m && !g) return fail(DFX_EINVAL, "dfx_row_norm_ba: m given without g output");
+    if ((dtype != DFX_BF16 && dtype != DFX_F16) || s == 0.0 || chunk_size % 64 != 0 ||
+        !dfx::norm_uses_tensor_cores(dtype, d_out, d_in, r))
+        return fail(DFX_EUNSUPPORTED, "dfx_row_norm_ba: needs the bf16 / fp16 tensor-core path");
+    dfx::NormArgs a{};
+    a.dt = dtype; a.w = W; a.a = A; a.b = B;
+    a.d_out = d_out; a.d_in = d_in; a.r = r; a.s = s; a.chunk_size = chunk_size;
+    if (terms) { a.base_sq = terms; a.cross = terms + d_out; a.ba_sq = terms + 2 * d_out; }
+    a.m = m; a.w_norm = w_norm; a.g = g;
+    a.round_dt = dtype; a.mag_dt = mag_dtype;
+    a.ba_given = ba_sq;
+    int launches = 0;
+    const cudaError_t e = dfx::launch_norm(a, &ctx->ws, stream, &launches);
+    ctx->launches += launches;
+    return finish_call(ctx, e, "dfx_row_norm_ba");
+}
+
 int dfx_norm_partial(dfx_ctx* ctx, dfx_dtype dtype, const void* W_k, const void* A_k,
                      const void* B, int64_t d_out, int64_t d_in_k, int64_t r, int64_t chunk_size,
                      float* gram, float* base_sq, float* cross, dfx_stream_t stream) {

@@ -94,9 +94,14 @@ struct NormArgs {
     // earlier call's base_sq output): the U kernel runs without its base_sq chain and the
     // finisher takes the cached value.  bf16 tensor-core path only.
     const float* base_cached;
+    // Split form for pipelined stacks (bf16 / fp16 tensor-core path): kNormAdapter computes
+    // only the adapter term ba_sq (Gram + V, no W) into `ba_sq`; a kNormFull call with
+    // ba_given runs only W.A^T (+ chain) and finishes with that ba_sq.  The two use disjoint
+    // workspace, so an adapter call may overlap a ba_given call of the same context.
+    const float* ba_given;
 };
 
-enum NormMode : int { kNormFull = 0, kNormPartial = 1, kNormFinish = 2 };
+enum NormMode : int { kNormFull = 0, kNormPartial = 1, kNormFinish = 2, kNormAdapter = 3 };
 
 // Per-launch device timing (dfx_profile_enable): launch sites bracket each kernel
 // with these; they are no-ops unless the calling thread is inside a call on a

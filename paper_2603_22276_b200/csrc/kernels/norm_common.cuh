@@ -20,7 +20,8 @@ enum WsSlot : int {
     kWsTerms = 6,      // base_sq/cross/ba_sq  [3][d_out]      (when caller wants none)
     kWsGramCount = 7,  // per-128-row-block tile counters of the fused finisher (zeroed)
     kWsScale = 8,      // fp16 V operand: 2^-e of the scaled Gram split (one float)
-    kWsCount = 9
+    kWsAdaptCount = 9, // per-128-row-block counters of the adapter-only call (kNormAdapter)
+    kWsCount = 10
 };
 
 struct FinishArgs {

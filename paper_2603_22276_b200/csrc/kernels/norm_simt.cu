@@ -302,6 +302,11 @@ cudaError_t launch_norm(const NormArgs& a, Workspace* ws, cudaStream_t st, int* 
     // the tensor-core chain walks 64-wide K blocks: chunk boundaries must align to them
     const int64_t tc_din = a.mode == kNormFinish ? 64 : a.d_in;  // finish reads no W
     const bool tc = a.chunk_size % 64 == 0 && norm_tc_supported(a.dt, a.d_out, tc_din, a.r);
+    if (a.mode == kNormAdapter || a.ba_given) {   // split form: tensor-core path only
+        if ((a.mode != kNormAdapter && a.mode != kNormFull) || !tc || a.s == 0.0)
+            return cudaErrorNotSupported;
+        return launch_norm_tc(a, ws, st, launches);
+    }
     if (a.base_cached) {   // only the tensor-core U kernel can drop its chain
         if (a.mode != kNormFull || !tc || a.s == 0.0) return cudaErrorNotSupported;
         return launch_norm_tc(a, ws, st, launches);

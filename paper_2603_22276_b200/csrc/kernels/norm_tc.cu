@@ -1386,7 +1386,7 @@ UPlan plan_u(int64_t d_out, int64_t r, int64_t kb_in, int64_t chunk_blocks, int6
 }
 
 NormPlan plan_norm(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, int sms,
-                   bool need_v) {
+                   bool need_v, bool force_serial = false) {
     const int64_t r_pad = (r + kBK - 1) / kBK * kBK;
     const int64_t m_tiles = (d_out + kBM - 1) / kBM;
     const int64_t kb_in = (d_in + kBK - 1) / kBK;
@@ -1449,7 +1449,7 @@ NormPlan plan_norm(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, i
         const double v = vgemm(sms, p.sb, p.b_ctas, p.v_gstat);
         p.cycles = g + p.u.cycles + v;
         best = p;
-        if (force_st == kSerial) return best;
+        if (force_st == kSerial || force_serial) return best;
     }
     for (int side : {8, 12, 20, 28, 36, 52, 74}) {
         if (side >= sms) break;
@@ -1515,7 +1515,12 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
     const int64_t n_chunks = (d_in + a.chunk_size - 1) / a.chunk_size;
     const int sms = ws_sm_count(ws);
 
-    const NormPlan plan = plan_norm(d_out, d_in, r, a.chunk_size, sms, !partial);
+    // split form: the adapter-only call (Gram + V on all of the budget's SMs, one stream) and
+    // the W call given ba_sq (W.A^T only) both plan serially
+    const bool adapter = a.mode == kNormAdapter;
+    const bool given = a.ba_given != nullptr;
+    const NormPlan plan = plan_norm(d_out, d_in, r, a.chunk_size, sms, !partial && !given,
+                                    adapter || given);
     const UPlan& u = plan.u;
     const bool forked = plan.strategy != kSerial;
     // side kernels occupy whole TPCs beside the 2-SM U pairs
@@ -1554,9 +1559,10 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
     // tile of each 128-row block runs the finisher for its rows; one counter per block.
     const bool fuse = norm_fuse_enabled();
     unsigned* counters = nullptr;
-    if (fuse) {
+    if (fuse || adapter) {
         counters = static_cast<unsigned*>(
-            ws_get_zeroed(ws, kWsGramCount, size_t(m_tiles) * sizeof(unsigned), &err));
+            ws_get_zeroed(ws, adapter ? kWsAdaptCount : kWsGramCount, size_t(m_tiles) * sizeof(unsigned),
+                          &err));
         if (err != cudaSuccess) return err;
     }
     FinishArgs f{};
@@ -1564,14 +1570,22 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
     if (a.base_cached) { f.base_part = a.base_cached; f.base_parts = 1; }
     f.cross_part = cross; f.cross_parts = u.ks * u.sp.ns;
     if (!partial) { f.ba_part = ba; f.ba_parts = plan.sb.ns; }
+    if (given) { f.ba_part = a.ba_given; f.ba_parts = 1; }
     f.d_out = d_out; f.two_s = 2.0 * a.s; f.s2 = a.s * a.s;
     f.base_sq = a.base_sq; f.cross = a.cross; f.ba_sq = a.ba_sq;
     f.round_dt = a.round_dt; f.w_norm = a.w_norm;
     f.m = a.m; f.mag_dt = a.mag_dt; f.g = a.m ? a.g : nullptr;
     if (partial) { f.w_norm = nullptr; f.g = nullptr; f.ba_sq = nullptr; }
-    const int fin_total = u.ks * u.sp.ns + (partial ? 0 : plan.sb.ns);
+    if (adapter) {
+        // the V tiles of each block sum its slices into ba_sq (fixed order, as the finisher)
+        FinishArgs fa{};
+        fa.ba_part = ba; fa.ba_parts = plan.sb.ns; fa.d_out = d_out; fa.ba_sq = a.ba_sq;
+        f = fa;
+    }
+    const int fin_total = adapter ? plan.sb.ns
+                                  : u.ks * u.sp.ns + ((partial || given) ? 0 : plan.sb.ns);
     auto set_fin = [&](TcParams& p) {
-        if (!fuse) return;
+        if (!fuse && !adapter) return;
         p.fin = f;
         p.fin_count = counters;
         p.fin_total = fin_total;
@@ -1709,6 +1723,11 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
 
     auto run = [&]() -> cudaError_t {
         cudaError_t e;
+        if (adapter) {
+            if ((e = launch_gram(st)) != cudaSuccess) return e;
+            return launch_v(st);
+        }
+        if (given) return launch_u();
         if (plan.strategy == kSerial) {
             if ((e = launch_gram(st)) != cudaSuccess) return e;
             if ((e = launch_u()) != cudaSuccess) return e;
@@ -1737,7 +1756,7 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
         return err;
     }
 
-    if (fuse) return cudaSuccess;
+    if (fuse || adapter) return cudaSuccess;
     if (launches) ++*launches;
     return launch_finish(f, st);
 }

@@ -1,9 +1,12 @@
 #!/bin/bash
-mkdir -p gpurun_out/ko
-run() { tag=$1; shift; env "$@" timeout 300 ncu --metrics gpu__time_duration.sum,gpc__cycles_elapsed.max,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active --clock-control none -k regex:"tc_pair_rowdot" --csv \
-     --log-file gpurun_out/ko/$tag.csv python scripts/profile_module.py --steps 3 $EXTRA > /dev/null 2>&1; }
-for ka in 1 2; do
-  run s_split_ka$ka DFX_PAIR_KA=$ka DFX_LIB=variants/libdfx_s_split.so
-  run b_split_ka$ka DFX_PAIR_KA=$ka DFX_LIB=variants/libdfx_b_split.so
+B="--steps 20 --warmup 5 --no-cpu-baseline --no-cpu-full-module --lora-steps 0 --variant-steps 0 --e2e-steps 2"
+timeout 300 python bench.py $B > /tmp/s.log 2>&1; echo "base train | $(tail -1 /tmp/s.log | cut -c 60-100)"
+for as in 12 20 28 40 60; do
+  timeout 300 python bench.py $B --split-adapter 1 --adapter-sms $as > /tmp/s.log 2>&1
+  echo "split train adapter-sms $as rc=$? | $(tail -1 /tmp/s.log | cut -c 60-100)"
 done
-EXTRA="--d-out 1024" run s_split_d1024 DFX_LIB=variants/libdfx_s_split.so
+timeout 300 python bench.py $B --mode infer > /tmp/s.log 2>&1; echo "base infer | $(tail -1 /tmp/s.log | cut -c 60-100)"
+for as in 20 28 40 60; do
+  timeout 300 python bench.py $B --mode infer --split-adapter 1 --adapter-sms $as > /tmp/s.log 2>&1
+  echo "split infer adapter-sms $as rc=$? | $(tail -1 /tmp/s.log | cut -c 60-100)"
+done

@@ -64,7 +64,7 @@ def load_peaks():
         return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
 
 
-TRAIN_NORM_SMS = 140   # the C2 training pipeline's norm SM budget (measured, DESIGN 5.3)
+TRAIN_NORM_SMS = 138   # the C2 training pipeline's norm SM budget (measured, DESIGN 5.3-5.4)
 
 
 def algorithmic(cfg):
@@ -1182,7 +1182,7 @@ def main():
                          "kernel or NCCL through torch.distributed)")
     ap.add_argument("--norm-sms", type=int, default=-1,
                     help="SM budget of the norm GEMMs in the pipelined graph (0 = all; default: "
-                         "140 for the training step, measured best of 104..148, 0 for inference)")
+                         "138 for the training step, measured best of 104..148, 0 for inference)")
     ap.add_argument("--split-adapter", type=int, default=0,
                     help="1: the pipelined graph computes each module's adapter term (ba_sq = "
                          "rowquad(B, A A^T), dfx_norm_adapter) one module ahead on a third stream "
@@ -1197,8 +1197,8 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.norm_sms < 0:   # measured: the budget helps the C2 training pipeline only
-        # (DESIGN 5.3, round 2: 140 keeps the all-SM W.A^T plan, 128 SMs, with the Gram on
-        # 12 side SMs, and switches the d_mag backward to its partitioned 256-byte slabs)
+        # (DESIGN 5.3-5.4, round 2: 138 keeps the all-SM W.A^T plan, 128 SMs, with the Gram
+        # on 10 side SMs, and switches the d_mag backward to its partitioned 256-byte slabs)
         args.norm_sms = TRAIN_NORM_SMS if (args.mode == "train" and args.config == "c2") else 0
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

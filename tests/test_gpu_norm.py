@@ -280,10 +280,10 @@ def test_sm_budget_plans(oracle, budget, d_out, d_in, r):
     dfx.close()
 
 
-@pytest.mark.parametrize("budget", [72, 104, 140])
+@pytest.mark.parametrize("budget", [72, 104, 138])
 def test_sm_budget_full_size_c2(oracle, budget):
-    """C2 at full size under the pipelined bench's budgets (140 = the training step's since
-    round 2: the all-SM W.A^T plan with the Gram on 12 side SMs and V after U; 104 / 72: the
+    """C2 at full size under the pipelined bench's budgets (138 = the training step's since
+    round 2: the all-SM W.A^T plan with the Gram on 10 side SMs and V after U; 104 / 72: the
     full-r 2-SM tiling beside the Gram and V): base_sq bitwise on every row."""
     import paper_2603_22276_b200 as P
     dfx = P.Dfx(0)

@@ -1640,6 +1640,9 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
             static const int wpf = env_int("DFX_W_PREFETCH", 0);   // K blocks of W warmed into L2 ahead
             p.w_prefetch = wpf;
             p.stages = stages_for_pair(u.sp.bn, u.nh, p.ka);
+            // DFX_PAIR_STAGES caps the ring (measurement: leaves shared memory for a co-resident CTA)
+            static const int cap_st = env_int("DFX_PAIR_STAGES", 0);
+            if (cap_st >= 2) p.stages = std::min(p.stages, cap_st);
             p.tiles = static_cast<int>(pm_tiles * u.sp.ns);
             const int pairs = std::min<int>(p.tiles, std::max(1, u.ctas / (2 * u.ks)));
             if (std::getenv("DFX_PLAN_PRINT"))

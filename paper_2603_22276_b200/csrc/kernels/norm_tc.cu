@@ -1382,6 +1382,28 @@ UPlan plan_u(int64_t d_out, int64_t r, int64_t kb_in, int64_t chunk_blocks, int6
             u.cycles = c1;
         }
     }
+    // DFX_U_KS / DFX_U_NH: measurement overrides of the K-split count and the UMMAs per K step
+    static const int force_ks = env_int("DFX_U_KS", 0), force_nh = env_int("DFX_U_NH", 0);
+    if (u.pair && (force_ks > 0 || force_nh > 0)) {
+        const int nh = force_nh > 0 ? force_nh : u.nh;
+        int ks = force_ks > 0 ? force_ks : u.ks;
+        ks = static_cast<int>(std::min<int64_t>(ks, n_chunks));
+        const int64_t chunks_per_split = (n_chunks + ks - 1) / ks;
+        u.kbps = static_cast<int>(chunks_per_split * chunk_blocks);
+        u.ks = static_cast<int>((kb_in + u.kbps - 1) / u.kbps);
+        if (nh == 2 && r > 256 && 2 * bnh <= 512) {
+            u.nh = 2;
+            u.sp = {1, u.ks, static_cast<int>(bnh)};
+            u.work = 2 * pm_tiles;
+        } else if (nh == 1) {
+            const int ns = static_cast<int>((r + 255) / 256) < 2 && r > 128 ? 2 : static_cast<int>((r + 255) / 256);
+            const int bn = static_cast<int>(((r + ns - 1) / ns + 31) / 32 * 32);
+            u.nh = 1;
+            u.sp = {ns, u.ks, bn};
+            u.work = 2 * pm_tiles * ns;
+        }
+        u.ctas = static_cast<int>(std::min<int64_t>(u.work * u.ks, budget));
+    }
     return u;
 }
 

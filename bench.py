@@ -402,10 +402,13 @@ def run_gpu(args, rank, world, local_rank, dist):
                 if i >= nbuf:
                     stream.wait_event(ev_comp[i - nbuf])
                 if split and args.only != "compose":
-                    if i + 1 < n:
+                    if i + 1 < n and args.adapter_first:
                         adapt(i + 1)
                     stream.wait_event(ev_adapt[i])
                     norm_w(b, sA)
+                    # created after the W part: U's CTAs claim their SMs first
+                    if i + 1 < n and not args.adapter_first:
+                        adapt(i + 1)
                 elif args.only != "compose":
                     norm(b, sA)
                 ev_norm[i].record(stream)
@@ -1188,6 +1191,8 @@ def main():
                          "rowquad(B, A A^T), dfx_norm_adapter) one module ahead on a third stream "
                          "and finishes the norm with dfx_row_norm_ba (measured slower at C2: "
                          "7.32k vs 7.94k training, 10.0k vs 11.8k inference; DESIGN 5.4)")
+    ap.add_argument("--adapter-first", type=int, default=0,
+                    help="--split-adapter: create module i+1's adapter before module i's W part")
     ap.add_argument("--adapter-sms", type=int, default=28,
                     help="--split-adapter: SMs the adapter GEMMs plan for beside the W part")
     ap.add_argument("--lora-steps", type=int, default=50,

@@ -40,6 +40,12 @@ constexpr int kLN = 256;                      // d_out columns per tile
 constexpr int kLK = 64;                       // K block: one 128-byte swizzle atom
 constexpr int kLSlice = 32;                   // epilogue column slice (64-byte swizzle)
 constexpr int kLThreads = 320;
+#ifndef DFX_LC_AHEAD
+#define DFX_LC_AHEAD 1
+#endif
+// base slices in flight ahead of the arithmetic (1 or 2; 2 measured no faster: 63.2 vs 62.9 us
+// at C2, the epilogue is issue-bound — ncu: 160 MB of DRAM traffic in 68 us)
+constexpr int kLBaseAhead = DFX_LC_AHEAD;
 constexpr int kWProd = 8, kWMma = 9;
 constexpr int kAStage = kLM * kLK * 2;        // 16 KiB of mid
 constexpr int kBStage = kLN * kLK * 2;        // 32 KiB of B
@@ -227,8 +233,11 @@ __global__ void __launch_bounds__(kLThreads, 1)
             for (int k = 0; k < 4; ++k)
                 v[k] = ldg_nc_v4(src + min(c0 + 8 * k, p.d_out - 8));
         };
-        uint4 bnext[4];
+        // base runs kLBaseAhead slices ahead of the arithmetic (the epilogue's HBM stream is
+        // latency-bound: each thread keeps its next slices' 64-byte pieces in flight)
+        uint4 bnext[4], bnext2[4];
         load_base(blockIdx.x, 0, bnext);
+        if (kLBaseAhead > 1) load_base(blockIdx.x, 1, bnext2);
         int local = 0, nslice = 0;
         for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++local) {
             const int32_t m0 = (t % p.m_tiles) * kLM, n0 = (t / p.m_tiles) * kLN;
@@ -255,8 +264,15 @@ __global__ void __launch_bounds__(kLThreads, 1)
                 uint4 bv[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) bv[k] = bnext[k];
-                if (cs < 3) load_base(t, cs + 1, bnext);
-                else load_base(t + gridDim.x, 0, bnext);
+                if (kLBaseAhead > 1) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) bnext[k] = bnext2[k];
+                    if (cs < 2) load_base(t, cs + 2, bnext2);
+                    else load_base(t + gridDim.x, cs - 2, bnext2);
+                } else {
+                    if (cs < 3) load_base(t, cs + 1, bnext);
+                    else load_base(t + gridDim.x, 0, bnext);
+                }
                 uint32_t acc[32];
                 tmem_ld_32x32b_x32(tmem_base + static_cast<uint32_t>(slot * kLN + cl) +
                                        (static_cast<uint32_t>(q * 32) << 16),

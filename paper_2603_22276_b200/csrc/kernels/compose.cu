@@ -38,6 +38,17 @@ namespace dfx {
 namespace {
 
 // ------------------------------------------------------------- vector helpers
+// Two independent RN fp32 products in one packed FMUL2 (sm_100 mul.rn.f32x2): bitwise two
+// __fmul_rn.  Used only where no add follows that ptxas could fuse with it.
+__device__ __forceinline__ void fmul2_rn(float a0, float a1, float b0, float b1, float& d0, float& d1) {
+    uint64_t a = (uint64_t(__float_as_uint(a1)) << 32) | __float_as_uint(a0);
+    uint64_t b = (uint64_t(__float_as_uint(b1)) << 32) | __float_as_uint(b0);
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    d0 = __uint_as_float(static_cast<uint32_t>(d));
+    d1 = __uint_as_float(static_cast<uint32_t>(d >> 32));
+}
+
 template <typename T> struct Vec;  // 16-byte packs
 template <> struct Vec<float> {
     static constexpr int N = 4;
@@ -408,11 +419,21 @@ __global__ void __launch_bounds__(SerialCfg<T, S, Wd>::kThreads, 1)
                 if (col_ok && row < rows) {
                     float fy[V], fl[V], fb[V];
                     Vec<T>::unpack(v, fy);
+#ifndef DFX_NO_FMUL2
+#pragma unroll
+                    for (int k = 0; k < V; k += 2) {   // packed: t = s*dy, d_lora = g*t, d_base = (g-1)*dy
+                        float t0, t1;
+                        fmul2_rn(sf, sf, fy[k], fy[k + 1], t0, t1);
+                        fmul2_rn(gv[k], gv[k + 1], t0, t1, fl[k], fl[k + 1]);
+                        fmul2_rn(gm1[k], gm1[k + 1], fy[k], fy[k + 1], fb[k], fb[k + 1]);
+                    }
+#else
 #pragma unroll
                     for (int k = 0; k < V; ++k) {
                         fl[k] = __fmul_rn(gv[k], __fmul_rn(sf, fy[k]));
                         fb[k] = __fmul_rn(gm1[k], fy[k]);
                     }
+#endif
                     st_stream(d_lora + row * d_out + j0, Vec<T>::pack(fl));
                     st_stream(d_base + row * d_out + j0, Vec<T>::pack(fb));
                 }

@@ -1204,7 +1204,10 @@ def main():
     if args.norm_sms < 0:   # measured: the budget helps the C2 training pipeline only
         # (DESIGN 5.3-5.4, round 2: 138 keeps the all-SM W.A^T plan, 128 SMs, with the Gram
         # on 10 side SMs, and switches the d_mag backward to its partitioned 256-byte slabs)
-        args.norm_sms = TRAIN_NORM_SMS if (args.mode == "train" and args.config == "c2") else 0
+        # C5 (the 448-module stack of smaller modules) trains fastest at 104: 5.8-6.0k vs
+        # 5.3k modules/s unbudgeted, 5.6k at 138 (profiles/r02_c5_budget_sweep.txt)
+        args.norm_sms = (TRAIN_NORM_SMS if args.config == "c2" else 104 if args.config == "c5" else 0) \
+            if args.mode == "train" else 0
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `python bench.py --gpus N` without a launcher: re-exec under torchrun, one rank per

@@ -65,6 +65,9 @@ def load_peaks():
 
 
 TRAIN_NORM_SMS = 138   # the C2 training pipeline's norm SM budget (measured, DESIGN 5.3-5.4)
+# (config, mode) -> the pipelined graph's norm SM budget when --norm-sms is not given
+NORM_SMS_DEFAULT = {("c2", "train"): TRAIN_NORM_SMS, ("c3", "train"): 120, ("c3", "infer"): 120,
+                    ("c5", "train"): 104}
 
 
 def algorithmic(cfg):
@@ -359,7 +362,7 @@ def run_gpu(args, rank, world, local_rank, dist):
         # the pipelined graph runs module i's compose beside module i+1's norm: leave the
         # compose kernels the SMs the norm GEMMs do not plan for (dfx_ctx_set_sm_budget).
         # A serial step (npipe == 1) gets the whole GPU for every kernel.
-        n = args.norm_sms if mode == args.mode else (TRAIN_NORM_SMS if mode == "train" else 0)
+        n = args.norm_sms if mode == args.mode else NORM_SMS_DEFAULT.get((args.config, mode), 0)
         dfx.set_sm_budget(n if npipe > 1 else 0)
 
     def build_pipelined(mode, n):
@@ -1204,10 +1207,11 @@ def main():
     if args.norm_sms < 0:   # measured: the budget helps the C2 training pipeline only
         # (DESIGN 5.3-5.4, round 2: 138 keeps the all-SM W.A^T plan, 128 SMs, with the Gram
         # on 10 side SMs, and switches the d_mag backward to its partitioned 256-byte slabs)
-        # C5 (the 448-module stack of smaller modules) trains fastest at 104: 5.8-6.0k vs
-        # 5.3k modules/s unbudgeted, 5.6k at 138 (profiles/r02_c5_budget_sweep.txt)
-        args.norm_sms = (TRAIN_NORM_SMS if args.config == "c2" else 104 if args.config == "c5" else 0) \
-            if args.mode == "train" else 0
+        # Other configs (measured, profiles/r02_c5_budget_sweep.txt, r02_cfg_budget_sweep.txt):
+        # C5, the 448-module stack of smaller modules, trains fastest at 104 (5.8-6.0k vs 5.3k
+        # modules/s unbudgeted); C3 (28672 x 8192) at 120-128 in both modes (2.34k vs 1.97k
+        # training, 3.80k vs 3.25k inference); C1 / C4 gain nothing measurable.
+        args.norm_sms = NORM_SMS_DEFAULT.get((args.config, args.mode), 0)
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `python bench.py --gpus N` without a launcher: re-exec under torchrun, one rank per

@@ -1435,17 +1435,20 @@ NormPlan plan_norm(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, i
         const int64_t kb = 2 * r_pad / kBK;
         sb = choose_split(m_tiles, r, kb, 1, budget);
         ctas = static_cast<int>(std::min<int64_t>(m_tiles * sb.ns, budget));
-        const double tile_g = std::max(double(kb) * 4.0 * std::max(120.0, 0.5 * sb.bn),
-                                       double(kb) * (16384.0 + sb.bn * 128.0) / 42.0) + 2500.0;
+        // calibrated on the B200 (round 2): the model's per-tile figures x 1.4-1.65 = the measured
+        // steady-state tile time (generic ~19.5k cycles, G-stationary ~14.5k per pair tile at
+        // r = 384), plus the G-stationary kernel's G-slice prologue (~15k cycles)
+        const double tile_g = 1.4 * (std::max(double(kb) * 4.0 * std::max(120.0, 0.5 * sb.bn),
+                                              double(kb) * (16384.0 + sb.bn * 128.0) / 42.0) + 2500.0);
         const double generic = double((m_tiles * sb.ns + ctas - 1) / ctas) * tile_g;
         const GstatShape gsh = gstat_shape(r);
         const int mode = v_gstat_mode();
         if (mode == 0 || gsh.bn == 0 || budget < 2 * gsh.nsl) return generic;
         const int pairs = std::min<int>(static_cast<int>(pm_tiles_n * gsh.nsl), budget / 2) / gsh.nsl * gsh.nsl;
         const int64_t kx = r_pad / kBK;
-        const double tile_s = std::max(double(kx) * 8.0 * 130.0, double(kx) * 16384.0 / 42.0) + 2500.0;
+        const double tile_s = 1.65 * (std::max(double(kx) * 8.0 * 130.0, double(kx) * 16384.0 / 42.0) + 2500.0);
         const double gstat = double((pm_tiles_n + pairs / gsh.nsl - 1) / (pairs / gsh.nsl)) * tile_s +
-                             double(kx) * gsh.bn * 128.0 / 42.0;
+                             2500.0 * double(kx);
         if (mode == 1 || gstat < generic) {
             gs = true;
             sb = {gsh.nsl, 1, gsh.bn};

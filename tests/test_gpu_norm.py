@@ -452,7 +452,7 @@ def _full_size_check(dfx, oracle, d_out, d_in, r, seed, n_rows=256, cs=None):
     return cs
 
 
-@pytest.mark.parametrize("budget", [0, 104])
+@pytest.mark.parametrize("budget", [0, 104, 120])
 def test_full_size_c3_four_chunks(oracle, budget):
     """BASELINE C3 (d_out = 28672, d_in = 8192, r = 384, bf16) at full size with the reference's
     own plan (2304, 4): K splits only on chunk boundaries, the base_sq chain reset every 2304

@@ -63,6 +63,8 @@ struct TcParams {
     int nh;                 // pair kernel: UMMAs per K step (N per CTA pair = nh * bn)
     int ka;                 // pair kernel: 64-wide K blocks ("atoms") per ring stage (1 or 2)
     int tma3d;              // pair kernel: tmx / tmy are K-atom 3-D maps, one TMA per operand per stage
+    int zsmem;              // pair kernel, one tile per CTA: the epilogue's B rows arrive by TMA
+                            // into a ring slot freed after the last K stage (tmz, 128B swizzle)
     const float* out_scale; // rowdot: multiply each row's sum by *out_scale (fp16 V: 2^-e)
     // Fused finisher (rowdot): every tile of a 128-row block counts itself in
     // fin_count[block]; the tile completing the block (fin_total tiles over U and V) runs
@@ -547,7 +549,7 @@ __global__ void __launch_bounds__(kEl == kF32 ? kThreads + 32 * (kSplitWarps - 2
 template <int kEl>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_pair_rowdot(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
-                   const TcParams p) {
+                   const __grid_constant__ CUtensorMap tmz, const TcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -563,7 +565,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty = pfull + p.stages;
     uint64_t* tmem_full = empty + p.stages;     // [2]
     uint64_t* tmem_empty = tmem_full + 2;       // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    uint64_t* zfull = tmem_empty + 2;           // the epilogue's B tile landed (p.zsmem)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(zfull + 1);
 
     const int warp = warp_id(), lane = lane_id();
     const uint32_t rank = cluster_ctarank();
@@ -595,6 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tmem_full[a], 1);
             mbar_init(&tmem_empty[a], 8);
         }
+        mbar_init(zfull, 1);
         fence_mbar_init();
     }
 #ifdef DFX_KO_TMEM
@@ -661,6 +665,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     DFX_TR(0, it);
                     if (++s == p.stages) { s = 0; ph ^= 1; }
+                }
+                if (p.zsmem) {
+                    // this CTA's B rows of the tile (bn_pair columns, 64-column SW128 boxes)
+                    // into the next ring slot once the tensor cores have released it
+                    mbar_wait(&empty[s], ph ^ 1);
+                    const int nbox = (bn_pair + kBK - 1) / kBK;
+                    mbar_arrive_expect_tx(zfull, static_cast<uint32_t>(nbox * kXStage));
+                    const int64_t zc = int64_t(t % p.n_split) * bn_pair;
+                    uint8_t* sz = smem + s * stage_bytes;
+                    for (int bx = 0; bx < nbox; ++bx)
+                        tma_load_2d(&tmz, zfull, sz + bx * kXStage, static_cast<int32_t>(zc + bx * kBK),
+                                    static_cast<int32_t>(m0), pol_y);
                 }
             }
         }
@@ -771,6 +787,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t trow = tmem_base + static_cast<uint32_t>(slot) * slot_cols +
                                   (static_cast<uint32_t>(q * 32) << 16);
             float acc = 0.0f;
+            if (p.zsmem) {
+                // B from the staged tile: row `row` of 64-column boxes, 16-byte chunk c of a
+                // box row at (c ^ (row & 7)) (the 128-byte swizzle), conflict-free like the chain
+                mbar_wait(zfull, 0);
+                const uint8_t* zslot = smem + (((local + 1) * nkb) % p.stages) * stage_bytes;  // slot after the tile
+                for (int c0 = 0; c0 < bn_pair; c0 += 32) {
+                    uint32_t u[32];
+                    tmem_ld_32x32b_x32(trow + c0, u);
+                    tmem_ld_wait();
+                    if (gm < p.M) {
+                        const uint8_t* zrow = zslot + (c0 / kBK) * kXStage + row * 128;
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            if (c0 + 8 * v < bn_pair && n0 + c0 + 8 * v < p.N) {
+                                const int ch = ((c0 % kBK) / 8 + v) ^ (row & 7);
+                                float z[8];
+                                unpack8<kEl>(*reinterpret_cast<const uint4*>(zrow + (ch << 4)), z);
+#pragma unroll
+                                for (int e = 0; e < 8; ++e)
+                                    acc = fmaf(__uint_as_float(u[8 * v + e]), z[e], acc);
+                            }
+                        }
+                    }
+                }
+            } else
 #ifdef DFX_KO_EPI
             if (bn_pair < 0)
 #endif
@@ -1138,8 +1179,8 @@ int pair_atoms(int nh, int64_t kb_per_split, int64_t total_kb) {
     return ka;
 }
 
-cudaError_t launch_tc_pair(const CUtensorMap& tx, const CUtensorMap& ty, TcParams p, int pairs,
-                           int ks, cudaStream_t st, const char* name, int el) {
+cudaError_t launch_tc_pair(const CUtensorMap& tx, const CUtensorMap& ty, const CUtensorMap& tz,
+                           TcParams p, int pairs, int ks, cudaStream_t st, const char* name, int el) {
     cudaError_t e;
     auto kern = el == kF16 ? tc_pair_rowdot<kF16> : tc_pair_rowdot<kBF16>;
     if ((e = ensure_max_dyn_smem(reinterpret_cast<const void*>(kern), kMaxSmem)) != cudaSuccess)
@@ -1165,7 +1206,7 @@ cudaError_t launch_tc_pair(const CUtensorMap& tx, const CUtensorMap& ty, TcParam
         cudaMemsetAsync(tp, 0, sizeof(g_trace), st);
     }
 #endif
-    e = cudaLaunchKernelEx(&cfg, kern, tx, ty, p);
+    e = cudaLaunchKernelEx(&cfg, kern, tx, ty, tz, p);
     prof_end(st);
     if (e != cudaSuccess) return e;
 #ifdef DFX_TRACE
@@ -1674,7 +1715,16 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
                 std::fprintf(stderr, "u plan: pairs %d ks %d kbps %d tiles %d n_split %d bn %d nh %d stages %d"
                              " strategy %d side %d sms %d\n", pairs, u.ks, u.kbps, p.tiles, p.n_split, p.bn,
                              p.nh, p.stages, int(plan.strategy), plan.side, sms);
-            e = launch_tc_pair(tw, ta, p, pairs, u.ks, st, "u_rowdot_tc", el);
+            // one tile per CTA and a ring slot that holds the tile's B rows: stage them by TMA
+            // for the epilogue (DFX_PAIR_ZSMEM=0 keeps per-thread loads from L2)
+            CUtensorMap tz = tw;
+            static const int zs = env_int("DFX_PAIR_ZSMEM", 1);
+            const int bn_pair = p.nh * p.bn;
+            const int stage_b = p.ka * (kXStage + p.nh * (p.bn / 2) * kBK * 2);
+            if (zs && p.tiles <= pairs && (bn_pair + kBK - 1) / kBK * kXStage <= stage_b &&
+                make_tmap_2d(&tz, el, a.b, d_out, r, r * 2, kBK, kBM, true) == cudaSuccess)
+                p.zsmem = 1;
+            e = launch_tc_pair(tw, ta, tz, p, pairs, u.ks, st, "u_rowdot_tc", el);
         } else {
             e = make_tmap_2d(&ta, el, a.a, r, d_in, d_in * 2, kBK, u.sp.bn, true);
             if (e != cudaSuccess) return e;

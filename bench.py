@@ -728,6 +728,17 @@ def run_gpu(args, rank, world, local_rank, dist):
                  "achieved_tflops": round(nf / (norm_wall_ms / 1e3) / 1e12, 1),
                  "frac_burst": round(nf / (norm_wall_ms / 1e3) / 1e12 / peak_tf_burst, 4),
                  "step_wall_us": round(step_wall_ms * 1e3, 2)}
+    # The whole step against its floors: the algorithmic bytes of every launch in one module
+    # over the HBM copy peak, and its tensor flops over the burst bf16 peak (the pipelined
+    # step overlaps the two, so the larger floor bounds it).
+    step_bytes = sum(alg[k][2] * v["launches_per_step"] for k, v in kernels.items() if k in alg)
+    step_flops = sum(alg[k][1] * v["launches_per_step"] for k, v in kernels.items() if k in alg)
+    step_us = ms / args.steps * 1e3      # one module per step on each rank
+    floor_us = max(step_bytes / (peaks_hbm * 1e9), step_flops / (peak_tf_burst * 1e12)) * 1e6
+    step_roof = {"bytes_per_step": int(step_bytes), "flops_per_step": step_flops,
+                 "hbm_floor_us": round(step_bytes / (peaks_hbm * 1e9) * 1e6, 2),
+                 "tensor_floor_us": round(step_flops / (peak_tf_burst * 1e12) * 1e6, 2),
+                 "step_us": round(step_us, 2), "frac_of_floor": round(floor_us / step_us, 4)}
     log(json.dumps(kernels))
     canary("profile")
 
@@ -828,7 +839,8 @@ def run_gpu(args, rank, world, local_rank, dist):
                                     f"module i+1's norm on a second stream" if npipe > 1
                                     else "serial"),
                        "norm_sm_budget": args.norm_sms if npipe > 1 else 0},
-            "roofline": roofline, "roofline_norm_stage": norm_roof, "kernels": kernels,
+            "roofline": roofline, "roofline_norm_stage": norm_roof, "roofline_step": step_roof,
+            "kernels": kernels,
             "variants": variants,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,

@@ -80,18 +80,27 @@ struct TcParams {
 // its group; true in all 128 threads of the CTA whose tile completed the group.  The last
 // arrival resets the counter, so the next launch (stream-ordered) starts from zero.
 // `flag` is a word of the CTA's barrier area (no static shared memory: the kernels use the
-// whole 227 KiB opt-in dynamically).
+// whole 227 KiB opt-in dynamically).  Ordering: the named barrier orders the 128 threads'
+// stores before thread 0's acq_rel atomic at GPU scope (cumulative release: the same
+// pattern as a CTA-wide semaphore), and the winner's acquire is ordered before the other
+// threads' loads by the second barrier; -DDFX_FENCE_ALL keeps a fence in every thread.
 __device__ __forceinline__ bool last_arrival(unsigned* count, int total, volatile uint32_t* flag) {
+#ifdef DFX_FENCE_ALL
     __threadfence();
+#endif
     named_bar_sync(1, 128);
     if (threadIdx.x == 0) {
-        const bool last = atomicAdd(count, 1u) + 1u == static_cast<unsigned>(total);
+        unsigned old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(count) : "memory");
+        const bool last = old + 1u == static_cast<unsigned>(total);
         if (last) atomicExch(count, 0u);
         *flag = last ? 1u : 0u;
     }
     named_bar_sync(1, 128);
     const bool last = *flag != 0;
+#ifdef DFX_FENCE_ALL
     if (last) __threadfence();
+#endif
     return last;
 }
 
@@ -102,14 +111,22 @@ __device__ __forceinline__ bool last_arrival(unsigned* count, int total, volatil
 #ifdef DFX_TRACE
 constexpr int kTrN = 128, kTrEv = 4, kTrCta = 148;
 __device__ unsigned long long g_trace[kTrCta][kTrEv][kTrN];
+// V (tc_pair_gstat) timeline per CTA: 0 entry, 1 after the cluster sync, 2 producer issued the
+// G slice, 3 MMA saw the G slice, 4 MMA saw the first B stage, 5 MMA issued the tile's last
+// commit, 6 epilogue had its B slice in registers, 7 epilogue saw the accumulator, 8 epilogue
+// stored ba_sq, 9 epilogue done (finisher included)
+constexpr int kVtrEv = 10;
+__device__ unsigned long long g_vtrace[kTrCta][kVtrEv];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
 #define DFX_TR(ev, i) do { if ((i) < kTrN && blockIdx.x < kTrCta) g_trace[blockIdx.x][ev][i] = gtimer(); } while (0)
+#define VTR(ev) do { if (blockIdx.x < kTrCta) g_vtrace[blockIdx.x][ev] = gtimer(); } while (0)
 #else
 #define DFX_TR(ev, i) do { } while (0)
+#define VTR(ev) do { } while (0)
 #endif
 
 __device__ __forceinline__ void unpack_bf16x8(const uint4& v, float (&f)[8]) {
@@ -874,6 +891,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // double-buffered in TMEM so a tile's epilogue (rowdot with B from L2, the fused finisher)
 // overlaps the next tile's UMMAs.  Operand traffic per pair tile: 2 x 16 KiB x kx of B, instead
 // of re-streaming the G slice (96 rows x 2 r_pad) with every tile as the generic V kernel does.
+constexpr int kGstatBars = 16;   // G-slice barrier groups (K atoms share one beyond 16)
+
 template <int kEl>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_pair_gstat(const __grid_constant__ CUtensorMap tmb, const __grid_constant__ CUtensorMap tmg,
@@ -890,8 +909,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty = full + p.stages;
     uint64_t* tmem_full = empty + p.stages;     // [2]
     uint64_t* tmem_empty = tmem_full + 2;       // [2]
-    uint64_t* gfull = tmem_empty + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gfull + 1);
+    uint64_t* gfull = tmem_empty + 2;           // [ngb] G slice atoms landed
+    const int gsz = (kx + kGstatBars - 1) / kGstatBars;    // K atoms per G barrier
+    const int ngb = (kx + gsz - 1) / gsz;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gfull + ngb);
 
     const int warp = warp_id(), lane = lane_id();
     const uint32_t rank = cluster_ctarank();
@@ -905,6 +926,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t slot_cols = static_cast<uint32_t>((p.bn + 31) / 32 * 32);
 
     if (threadIdx.x == 0) {
+        VTR(0);
         tma_prefetch_desc(&tmb);
         tma_prefetch_desc(&tmg);
         for (int s = 0; s < p.stages; ++s) {
@@ -915,7 +937,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tmem_full[a], 1);
             mbar_init(&tmem_empty[a], 8);
         }
-        mbar_init(gfull, 1);
+        for (int g = 0; g < ngb; ++g) mbar_init(&gfull[g], 1);
         fence_mbar_init();
     }
     if (warp == kWarpMma) tmem_alloc_pair<512>(tmem_slot);
@@ -924,34 +946,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) VTR(1);
 
     if (warp == kWarpProducer) {
         if (lane == 0) {
             const uint64_t pol = policy_evict_last();
-            // the resident G slice: this CTA's half_n rows, hi atoms then lo atoms
-            if (leader) mbar_arrive_expect_tx(gfull, 2u * 2u * kx * g_atom);
-            const uint32_t gbar = mapa_shared(smem_u32(gfull), 0);
-            for (int a = 0; a < 2 * kx; ++a)
-                tma_load_2d_pair(&tmg, gbar, sg + a * g_atom, a * kBK,
-                                 static_cast<int32_t>(n0 + int64_t(rank) * half_n), pol);
+            // The resident G slice (this CTA's half_n rows; hi atoms 0..kx-1, lo atoms kx..):
+            // atom a of G_hi and G_lo ahead of the first tile's B atom a, each group of atoms
+            // on its own barrier, so the first UMMAs start when their operands land instead
+            // of after the whole slice.
             int s = 0;
             uint32_t ph = 0;
+            int g_next = 0;                       // next G barrier group to issue
+            auto issue_g = [&](int upto) {        // G atoms of the groups covering K atoms < upto
+                for (; g_next < ngb && g_next * gsz < upto; ++g_next) {
+                    const int a0 = g_next * gsz, a1 = a0 + gsz < kx ? a0 + gsz : kx;
+                    if (leader) mbar_arrive_expect_tx(&gfull[g_next], 2u * 2u * (a1 - a0) * g_atom);
+                    const uint32_t gbar = mapa_shared(smem_u32(&gfull[g_next]), 0);
+                    for (int a = a0; a < a1; ++a)
+                        for (int hl = 0; hl < 2; ++hl)
+                            tma_load_2d_pair(&tmg, gbar, sg + (hl * kx + a) * g_atom, (hl * kx + a) * kBK,
+                                             static_cast<int32_t>(n0 + int64_t(rank) * half_n), pol);
+                }
+            };
+            bool first_tile = true;
             for (int t = first; t < p.tiles; t += pps) {
                 const int64_t m0 = int64_t(t) * (2 * kBM) + int64_t(rank) * kBM;
                 for (int a = 0; a < kx; ++a) {
+                    if (first_tile) issue_g(a + 1);
+                    if (first_tile && a == 0) VTR(2);
                     mbar_wait(&empty[s], ph ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[s], 2 * kXStage);
                     tma_load_2d_pair(&tmb, mapa_shared(smem_u32(&full[s]), 0), sb + s * kXStage,
                                      a * kBK, static_cast<int32_t>(m0), pol);
                     if (++s == p.stages) { s = 0; ph ^= 1; }
                 }
+                first_tile = false;               // (a pair with no tile loads no G)
             }
         }
     } else if (warp == kWarpMma) {
         if (leader && lane == 0) {
             const uint32_t idesc = umma_idesc_f16(ab_fmt(kEl), 2 * kBM, static_cast<uint32_t>(p.bn));
-            mbar_wait(gfull, 0);
-            tc_fence_after();
             int s = 0;
             uint32_t ph = 0;
             int local = 0;
@@ -961,7 +996,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&tmem_empty[slot], ((local >> 1) & 1) ^ 1);
                 tc_fence_after();
                 for (int a = 0; a < kx; ++a) {
+                    if (local == 0) {
+                        mbar_wait(&gfull[a / gsz], 0);   // G atoms of this K range (first tile)
+                        if (a == 0) VTR(3);
+                    }
                     mbar_wait(&full[s], ph);
+                    if (local == 0 && a == 0) VTR(4);
                     tc_fence_after();
                     const uint32_t bx = smem_u32(sb + s * kXStage);
                     for (int hl = 0; hl < 2; ++hl) {
@@ -975,6 +1015,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (++s == p.stages) { s = 0; ph ^= 1; }
                 }
                 umma_commit_pair_mc(&tmem_full[slot], 0x3);
+                VTR(5);
             }
         }
     } else if (warp < 4) {
@@ -996,7 +1037,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     zb[v] = (gm < p.M && 8 * v < p.bn && n0 + 8 * v < p.N)
                                 ? *reinterpret_cast<const uint4*>(zr + 8 * v) : make_uint4(0, 0, 0, 0);
             }
+#ifdef DFX_TRACE
+            if (threadIdx.x == 0) { uint32_t x = 0; for (int v = 0; v < 32; ++v) x ^= zb[v].x; if (x == 0x9e3779b9u) g_vtrace[0][0] = 0; VTR(6); }
+#endif
             mbar_wait(&tmem_full[slot], (local >> 1) & 1);
+            if (threadIdx.x == 0) VTR(7);
             tc_fence_after();
             const uint32_t trow = tmem_base + static_cast<uint32_t>(slot) * slot_cols +
                                   (static_cast<uint32_t>(q * 32) << 16);
@@ -1026,8 +1071,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (p.out_scale) acc = __fmul_rn(acc, *p.out_scale);   // exact power of two
             if (gm < p.M) p.out[int64_t(slice) * p.M + gm] = acc;
+            if (threadIdx.x == 0) VTR(8);
             if (p.fin_count && m0 < p.M && last_arrival(p.fin_count + m0 / kBM, p.fin_total, tmem_slot + 1) && gm < p.M)
                 finish_row(p.fin, gm);
+            if (threadIdx.x == 0) VTR(9);
         }
     }
     tc_fence_before();
@@ -1332,7 +1379,7 @@ struct NormPlan {
 struct GstatShape { int bn, nsl, stages; };
 
 size_t smem_for_gstat(int bn, int64_t r_pad, int stages) {
-    return size_t(2 * (r_pad / kBK)) * (bn / 2) * kBK * 2 + size_t(stages) * kXStage + 1024 + 256;
+    return size_t(2 * (r_pad / kBK)) * (bn / 2) * kBK * 2 + size_t(stages) * kXStage + 1024 + 512;
 }
 
 GstatShape gstat_shape(int64_t r) {
@@ -1371,9 +1418,30 @@ cudaError_t launch_gstat(const CUtensorMap& tb, const CUtensorMap& tg, const TcP
     cfg.attrs = at;
     cfg.numAttrs = 1;
     prof_begin("ba_rowdot_tc", st);
+#ifdef DFX_TRACE
+    const char* trace_file = std::getenv("DFX_VTRACE");
+    if (trace_file) {
+        void* tp = nullptr;
+        cudaGetSymbolAddress(&tp, g_vtrace);
+        cudaMemsetAsync(tp, 0, sizeof(g_vtrace), st);
+    }
+#endif
     e = cudaLaunchKernelEx(&cfg, kern, tb, tg, p);
     prof_end(st);
     if (e != cudaSuccess) return e;
+#ifdef DFX_TRACE
+    if (trace_file) {
+        static unsigned long long host[kTrCta][kVtrEv];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(host, g_vtrace, sizeof(host));
+        if (FILE* f = std::fopen(trace_file, "ab")) {
+            const int hdr[8] = {2 * pairs, p.stages, p.ka, p.bn, p.n_split, p.tiles, 0, 0};
+            std::fwrite(hdr, sizeof(hdr), 1, f);
+            std::fwrite(host, sizeof(host), 1, f);
+            std::fclose(f);
+        }
+    }
+#endif
     return cudaGetLastError();
 }
 
@@ -1476,9 +1544,10 @@ NormPlan plan_norm(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, i
         const int64_t kb = 2 * r_pad / kBK;
         sb = choose_split(m_tiles, r, kb, 1, budget);
         ctas = static_cast<int>(std::min<int64_t>(m_tiles * sb.ns, budget));
-        // calibrated on the B200 (round 2): the model's per-tile figures x 1.4-1.65 = the measured
-        // steady-state tile time (generic ~19.5k cycles, G-stationary ~14.5k per pair tile at
-        // r = 384), plus the G-stationary kernel's G-slice prologue (~15k cycles)
+        // calibrated on the B200 (round 2): the model's per-tile figures x 1.4-1.5 ~ the measured
+        // steady-state tile times (generic ~19.5k cycles, G-stationary ~13-14.5k per pair tile
+        // at r = 384), plus the G-stationary kernel's G-slice prologue; at C2 on all SMs the
+        // G-stationary kernel measures 15.6 vs 16.7 us (ncu) and is the one chosen
         const double tile_g = 1.4 * (std::max(double(kb) * 4.0 * std::max(120.0, 0.5 * sb.bn),
                                               double(kb) * (16384.0 + sb.bn * 128.0) / 42.0) + 2500.0);
         const double generic = double((m_tiles * sb.ns + ctas - 1) / ctas) * tile_g;
@@ -1487,9 +1556,9 @@ NormPlan plan_norm(int64_t d_out, int64_t d_in, int64_t r, int64_t chunk_size, i
         if (mode == 0 || gsh.bn == 0 || budget < 2 * gsh.nsl) return generic;
         const int pairs = std::min<int>(static_cast<int>(pm_tiles_n * gsh.nsl), budget / 2) / gsh.nsl * gsh.nsl;
         const int64_t kx = r_pad / kBK;
-        const double tile_s = 1.65 * (std::max(double(kx) * 8.0 * 130.0, double(kx) * 16384.0 / 42.0) + 2500.0);
+        const double tile_s = 1.5 * (std::max(double(kx) * 8.0 * 130.0, double(kx) * 16384.0 / 42.0) + 2500.0);
         const double gstat = double((pm_tiles_n + pairs / gsh.nsl - 1) / (pairs / gsh.nsl)) * tile_s +
-                             2500.0 * double(kx);
+                             1000.0 * double(kx);
         if (mode == 1 || gstat < generic) {
             gs = true;
             sb = {gsh.nsl, 1, gsh.bn};

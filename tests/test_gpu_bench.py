@@ -27,5 +27,7 @@ def test_bench_short_run(dfx, mode):
     assert KEYS <= set(line), KEYS - set(line)
     assert line["value"] > 0 and line["gpu_launches"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    st = line["roofline_step"]
+    assert st["bytes_per_step"] > 0 and 0 < st["frac_of_floor"] <= 1.0, st
     canaries = [l for l in (r.stdout + r.stderr).splitlines() if "canary after" in l]
     assert canaries and all(l.rstrip().endswith("ok") for l in canaries), canaries

@@ -383,6 +383,8 @@ __global__ void __launch_bounds__(SerialCfg<T, S, Wd>::kThreads, 1)
                     for (int c = 0; c < P; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(fy[c], fi[c]));
                 }
             }
+            // every word read from the slot fed the chain above before this release, so the
+            // reads are complete when the TMA may refill it (no proxy fence needed)
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
         }

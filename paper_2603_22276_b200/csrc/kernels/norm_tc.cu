@@ -247,6 +247,11 @@ __device__ __forceinline__ void chain_tile(const ChainUnits& cu, const uint8_t* 
         }
         kpos += kIsF32 ? 32 : 64;
         }
+        // The release lets the TMA (async proxy) refill the slot.  Every loaded word fed the
+        // FADD chain above, and in-order issue puts the arrive after those FADDs, which wait
+        // for the loads' data: the generic reads are complete before the release, so no
+        // fence.proxy.async is needed here (a ring whose reads are NOT consumed before the
+        // release needs one: profiles/r02_lora_tma_base.txt).
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         if (++s == stages) { s = 0; ph ^= 1; }

@@ -24,10 +24,16 @@
 // Warp roles (320 threads): 0-7 epilogue (warp w owns TMEM lane quadrant w % 4, warps
 // 0-3 take column slices 0-1 of a tile, warps 4-7 slices 2-3), 8 operand producer,
 // 9 MMA issuer.
+//
+// Measured alternatives kept as compile-time switches, all parity-green and all slower at C2
+// (profiles/r02_lora_epilogue_sweep.txt): DFX_LC_EPI_WARPS=16, DFX_LC_PAIR=1 (CTA pairs, half
+// of B per CTA), DFX_LC_GSTORE=1 (one 128-row TMA store per column group).  Knock-out
+// switches DFX_LC_KO_{BASE,STORE,MMA,EPI} split the kernel's time.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "launch.h"
 #include "ptx.cuh"
@@ -39,17 +45,48 @@ constexpr int kLM = 128;                      // token rows per tile
 constexpr int kLN = 256;                      // d_out columns per tile
 constexpr int kLK = 64;                       // K block: one 128-byte swizzle atom
 constexpr int kLSlice = 32;                   // epilogue column slice (64-byte swizzle)
-constexpr int kLThreads = 320;
-#ifndef DFX_LC_AHEAD
-#define DFX_LC_AHEAD 1
+#ifndef DFX_LC_EPI_WARPS
+#define DFX_LC_EPI_WARPS 8
 #endif
-// base slices in flight ahead of the arithmetic (1 or 2; 2 measured no faster: 63.2 vs 62.9 us
-// at C2, the epilogue is issue-bound — ncu: 160 MB of DRAM traffic in 68 us)
-constexpr int kLBaseAhead = DFX_LC_AHEAD;
-constexpr int kWProd = 8, kWMma = 9;
+constexpr int kEpiWarps = DFX_LC_EPI_WARPS;           // 8 or 16 epilogue warps
+constexpr int kGroups = kEpiWarps / 4;                // column groups (4 TMEM lane quadrants each)
+constexpr int kLThreads = (kEpiWarps + 2) * 32;
+#ifndef DFX_LC_SLEEP
+#define DFX_LC_SLEEP 128
+#endif
+// back-off of the producer / MMA warps' barrier waits (ns; 0 = spin): the kernel is bounded by
+// the epilogue's instruction issue, and a spinning try_wait loop takes issue slots on the
+// schedulers it shares with epilogue warps
+constexpr uint32_t kLSleepNs = DFX_LC_SLEEP;
+__device__ __forceinline__ void lc_wait(uint64_t* bar, uint32_t phase) {
+    if (kLSleepNs) mbar_wait_sleep(bar, phase, kLSleepNs);
+    else mbar_wait(bar, phase);
+}
+constexpr int kWProd = kEpiWarps, kWMma = kEpiWarps + 1;
 constexpr int kAStage = kLM * kLK * 2;        // 16 KiB of mid
-constexpr int kBStage = kLN * kLK * 2;        // 32 KiB of B
+#ifndef DFX_LC_PAIR
+#define DFX_LC_PAIR 0
+#endif
+#ifndef DFX_LC_GSTORE
+#define DFX_LC_GSTORE 0
+#endif
+// group stores: the four warps of a column group stage one 128-row slice together and one
+// thread issues a single 128 x 32 TMA store per output (instead of one 32 x 32 store per
+// warp): the TMA engine's per-instruction cost, not bytes, paced the epilogue's stores
+constexpr bool kGStore = DFX_LC_GSTORE != 0;
+// CTA pairs (cta_group::2): a cluster of two CTAs owns a 256-token x 256-column tile, each CTA
+// staging its own 128 mid rows and HALF of the tile's B rows; the leader issues M = 256 UMMAs
+// that read both CTAs' shared memory and accumulate into both CTAs' TMEM (each its own 128
+// rows).  Per SM, B traffic through shared memory halves (the kernel is bound by its shared-
+// memory traffic: operand TMA writes + tensor-core reads + output staging).
+constexpr bool kPair = DFX_LC_PAIR != 0;
+constexpr int kBRows = kPair ? kLN / 2 : kLN;      // B rows per CTA per stage
+constexpr int kBStage = kBRows * kLK * 2;          // 16 KiB (pair) / 32 KiB of B
+constexpr int kTileM = kPair ? 2 * kLM : kLM;      // token rows per (pair) tile
+constexpr int kMaxStages = kPair ? 6 : 4;
 constexpr int kSlice = kLM * kLSlice * 2;     // 8 KiB
+constexpr int kWCols = kLN / kGroups;         // columns of a tile per epilogue warp
+constexpr int kWSlices = kWCols / kLSlice;    // 32-column slices per warp and tile
 constexpr int kMaxOut = 4;                    // y, delta, inner, lora
 
 struct LcMaps {
@@ -62,6 +99,7 @@ struct LcParams {
     int kb;                 // K blocks (ceil(r / 64))
     int m_tiles, tiles;
     int stages;
+    int nbuf;               // output staging buffers per group (2: double-buffered)
     int n_out;              // enabled outputs, compacted in out[] / the smem buffers
     int slot[kMaxOut];      // kind (0 y, 1 delta, 2 inner, 3 lora) -> buffer index, -1 = off
     float s;
@@ -81,6 +119,9 @@ __device__ __forceinline__ void tma_store_2d(const void* desc, const void* smem_
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() {
     asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() {
@@ -128,22 +169,28 @@ template <> struct LcT<__half> {
     }
 };
 
-template <typename T>
+template <typename T, bool kBias>
 __global__ void __launch_bounds__(kLThreads, 1)
     lora_compose_kernel(const __grid_constant__ LcMaps maps, const LcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     constexpr int kStage = kAStage + kBStage;
-    uint8_t* s_out = smem + p.stages * kStage;           // [2 groups][2 buffers][n_out][8 KiB]
-    uint64_t* full = reinterpret_cast<uint64_t*>(s_out + 4 * p.n_out * kSlice);
+    uint8_t* s_out = smem + p.stages * kStage;   // [kGroups][nbuf buffers][n_out][8 KiB]
+    uint64_t* full = reinterpret_cast<uint64_t*>(s_out + kGroups * p.nbuf * p.n_out * kSlice);
     uint64_t* empty = full + p.stages;
     uint64_t* tmem_full = empty + p.stages;      // [2]
     uint64_t* tmem_empty = tmem_full + 2;        // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
-    __shared__ __align__(16) float s_gw[8][3][kLN / 2];   // epilogue warp: g, g - 1, bias
+    __shared__ __align__(16) float s_gw[kEpiWarps][3][kWCols];   // epilogue warp: g, g - 1, bias
     const int warp = warp_id(), lane = lane_id();
+    const uint32_t rank = kPair ? cluster_ctarank() : 0;
+    const bool leader = rank == 0;
+    const int unit = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+    const int nunits = kPair ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+    // this CTA's first token row of tile t (its half of a pair tile)
+    auto tile_m0 = [&](int t) { return (t % p.m_tiles) * kTileM + static_cast<int>(rank) * kLM; };
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.stages; ++i) {
             mbar_init(&full[i], 1);
@@ -151,13 +198,17 @@ __global__ void __launch_bounds__(kLThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tmem_full[i], 1);
-            mbar_init(&tmem_empty[i], 8);
+            mbar_init(&tmem_empty[i], kPair ? 2 * kEpiWarps : kEpiWarps);   // leader's counts both
         }
         fence_mbar_init();
     }
-    if (warp == kWMma) tmem_alloc<512>(tmem_slot);
+    if (warp == kWMma) {
+        if (kPair) tmem_alloc_pair<512>(tmem_slot);
+        else tmem_alloc<512>(tmem_slot);
+    }
     tc_fence_before();
     __syncthreads();
+    if (kPair) cluster_sync();      // the peer's barriers exist before any cross-CTA arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -169,134 +220,164 @@ __global__ void __launch_bounds__(kLThreads, 1)
             const uint64_t pol = policy_evict_last();   // mid and B are re-read across tiles
             int s = 0;
             uint32_t ph = 0;
-            for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
-                const int32_t m0 = (t % p.m_tiles) * kLM, n0 = (t / p.m_tiles) * kLN;
+            for (int t = unit; t < p.tiles; t += nunits) {
+                const int32_t m0 = tile_m0(t);
+                const int32_t n0 = (t / p.m_tiles) * kLN + static_cast<int>(rank) * kBRows;
                 for (int kb = 0; kb < p.kb; ++kb) {
-                    mbar_wait(&empty[s], ph ^ 1);
-                    mbar_arrive_expect_tx(&full[s], kStage);
+                    lc_wait(&empty[s], ph ^ 1);
                     uint8_t* sa = smem + s * kStage;
-                    tma_load_2d(&maps.mid, &full[s], sa, kb * kLK, m0, pol);
-                    tma_load_2d(&maps.b, &full[s], sa + kAStage, kb * kLK, n0, pol);
+                    if (kPair) {
+                        // both CTAs' loads complete on the leader's barrier
+                        if (leader) mbar_arrive_expect_tx(&full[s], 2 * kStage);
+                        const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
+                        tma_load_2d_pair(&maps.mid, lbar, sa, kb * kLK, m0, pol);
+                        tma_load_2d_pair(&maps.b, lbar, sa + kAStage, kb * kLK, n0, pol);
+                    } else {
+                        mbar_arrive_expect_tx(&full[s], kStage);
+                        tma_load_2d(&maps.mid, &full[s], sa, kb * kLK, m0, pol);
+                        tma_load_2d(&maps.b, &full[s], sa + kAStage, kb * kLK, n0, pol);
+                    }
                     if (++s == p.stages) { s = 0; ph ^= 1; }
                 }
             }
         }
     } else if (warp == kWMma) {
         // ================= MMA issuer (single thread) =================
-        if (lane == 0) {
-            const uint32_t idesc = umma_idesc_f16(p.fp16 ? 0u : 1u, kLM, kLN);
+        if (lane == 0 && leader) {
+            const uint32_t idesc = umma_idesc_f16(p.fp16 ? 0u : 1u, kTileM, kLN);
             int s = 0;
             uint32_t ph = 0;
             int local = 0;
-            for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++local) {
+            for (int t = unit; t < p.tiles; t += nunits, ++local) {
                 const int slot = local & 1;
                 const uint32_t tacc = tmem_base + static_cast<uint32_t>(slot * kLN);
-                mbar_wait(&tmem_empty[slot], ((local >> 1) & 1) ^ 1);
+                lc_wait(&tmem_empty[slot], ((local >> 1) & 1) ^ 1);
                 tc_fence_after();
                 for (int kb = 0; kb < p.kb; ++kb) {
-                    mbar_wait(&full[s], ph);
+                    lc_wait(&full[s], ph);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + s * kStage);
                     const uint32_t sb = sa + kAStage;
+#ifndef DFX_LC_KO_MMA
 #pragma unroll
-                    for (int k = 0; k < kLK / 16; ++k)
-                        umma_f16(tacc, umma_desc_k_sw128(sa + k * 32), umma_desc_k_sw128(sb + k * 32),
-                                 idesc, (kb > 0 || k > 0) ? 1u : 0u);
-                    umma_commit(&empty[s]);
+                    for (int k = 0; k < kLK / 16; ++k) {
+                        const uint64_t ad = umma_desc_k_sw128(sa + k * 32);
+                        const uint64_t bd = umma_desc_k_sw128(sb + k * 32);
+                        if (kPair) umma_f16_pair(tacc, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                        else umma_f16(tacc, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                    }
+#else
+                    (void)sb; (void)tacc;
+#endif
+                    if (kPair) umma_commit_pair_mc(&empty[s], 0x3);
+                    else umma_commit(&empty[s]);
                     if (++s == p.stages) { s = 0; ph ^= 1; }
                 }
-                umma_commit(&tmem_full[slot]);
+                if (kPair) umma_commit_pair_mc(&tmem_full[slot], 0x3);
+                else umma_commit(&tmem_full[slot]);
             }
         }
-    } else if (warp < 8) {
+    } else if (warp < kEpiWarps) {
         // ================= epilogue: one token row per thread =================
         // Warp w (TMEM lane quadrant q = w % 4) owns the 32 rows 32q.. of each tile and the
-        // column half grp = w / 4, in four 32-column slices.  Each slice's outputs go to the
-        // warp's part of a double-buffered 64-byte-swizzled smem slice and leave by the
-        // warp's own TMA store (32 x 32 box) while the next slice computes: no cross-warp
-        // synchronisation in the epilogue.
+        // kWCols columns of group grp = w / 4, in 32-column slices.  Each slice's outputs go
+        // to the warp's part of a (double-buffered where shared memory allows) 64-byte-
+        // swizzled smem slice and leave by the warp's own TMA store (32 x 32 box) while the
+        // next slice computes: no cross-warp synchronisation in the epilogue.
         const int grp = warp >> 2, q = warp & 3;
         const int row = q * 32 + lane;
         const int sw = (row >> 1) & 3;                          // SWIZZLE_64B chunk XOR
-        uint8_t* obase = s_out + grp * 2 * p.n_out * kSlice;    // [2 buffers][n_out][slice]
-        float (*gw)[kLN / 2] = s_gw[warp];                      // [g | g - 1 | bias][column]
+        uint8_t* obase = s_out + grp * p.nbuf * p.n_out * kSlice;  // [nbuf][n_out][slice]
+        float (*gw)[kWCols] = s_gw[warp];                       // [g | g - 1 | bias][column]
         const float sf = p.s;
         // this thread's 64-byte base piece of a slice (row clamped in the token tail, columns
         // in the d_out tail; those outputs are clipped by the TMA store), read through L1
         // one slice ahead so the DRAM latency hides behind the current slice's arithmetic
+        // (two slices or a whole tile ahead measured no faster)
         auto load_base = [&](int tt, int cs, uint4 (&v)[4]) {
             if (tt >= p.tiles) return;
-            const int64_t r0 = min(int64_t((tt % p.m_tiles) * kLM + row), p.rows - 1);
-            const int64_t c0 = int64_t(tt / p.m_tiles) * kLN + 128 * grp + kLSlice * cs;
+            const int64_t r0 = min(int64_t(tile_m0(tt) + row), p.rows - 1);
+            const int64_t c0 = int64_t(tt / p.m_tiles) * kLN + kWCols * grp + kLSlice * cs;
             const T* src = static_cast<const T*>(p.base) + r0 * p.d_out;
+#ifdef DFX_LC_KO_BASE
+            v[0] = v[1] = v[2] = v[3] = make_uint4(0, 0, 0, 0);   // knock-out: no base stream
+            (void)src; (void)c0;
+#else
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 v[k] = ldg_nc_v4(src + min(c0 + 8 * k, p.d_out - 8));
+#endif
         };
-        // base runs kLBaseAhead slices ahead of the arithmetic (the epilogue's HBM stream is
-        // latency-bound: each thread keeps its next slices' 64-byte pieces in flight)
-        uint4 bnext[4], bnext2[4];
-        load_base(blockIdx.x, 0, bnext);
-        if (kLBaseAhead > 1) load_base(blockIdx.x, 1, bnext2);
+        uint4 bnext[4];
+        load_base(unit, 0, bnext);
         int local = 0, nslice = 0;
-        for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++local) {
-            const int32_t m0 = (t % p.m_tiles) * kLM, n0 = (t / p.m_tiles) * kLN;
-            // g, g - 1 and bias for the warp's 128 columns (a missing bias is -0.0, an exact
+        for (int t = unit; t < p.tiles; t += nunits, ++local) {
+            const int32_t m0 = tile_m0(t), n0 = (t / p.m_tiles) * kLN;
+            // g, g - 1 and bias for the warp's columns (a missing bias is -0.0, an exact
             // no-op in the fp32 add; columns past d_out are clamped, their outputs clipped)
             {
-                const int64_t j = min(int64_t(n0 + 128 * grp + 4 * lane), p.d_out - 4);
-                const float4 gv4 = __ldg(reinterpret_cast<const float4*>(p.g + j));
-                const float4 bv4 = p.bias ? __ldg(reinterpret_cast<const float4*>(p.bias + j))
-                                          : make_float4(-0.0f, -0.0f, -0.0f, -0.0f);
-                reinterpret_cast<float4*>(gw[0])[lane] = gv4;
-                reinterpret_cast<float4*>(gw[1])[lane] =
-                    make_float4(__fsub_rn(gv4.x, 1.0f), __fsub_rn(gv4.y, 1.0f),
-                                __fsub_rn(gv4.z, 1.0f), __fsub_rn(gv4.w, 1.0f));
-                reinterpret_cast<float4*>(gw[2])[lane] = bv4;
+                constexpr int kPer = kWCols / 32;                // 4 (8 warps) or 2 (16 warps)
+                const int64_t j = min(int64_t(n0 + kWCols * grp + kPer * lane), p.d_out - kPer);
+#pragma unroll
+                for (int i = 0; i < kPer; ++i) {
+                    const float gv = __ldg(p.g + j + i);
+                    gw[0][kPer * lane + i] = gv;
+                    gw[1][kPer * lane + i] = __fsub_rn(gv, 1.0f);
+                    gw[2][kPer * lane + i] = kBias ? __ldg(p.bias + j + i) : -0.0f;
+                }
             }
             __syncwarp();
             const int slot = local & 1;
             mbar_wait(&tmem_full[slot], (local >> 1) & 1);
             tc_fence_after();
-            for (int cs = 0; cs < 4; ++cs, ++nslice) {
-                const int cl = 128 * grp + kLSlice * cs;        // slice's first column in the tile
+#pragma unroll
+            for (int cs = 0; cs < kWSlices; ++cs, ++nslice) {
+                const int cl = kWCols * grp + kLSlice * cs;     // slice's first column in the tile
                 const int col0 = n0 + cl;
                 uint4 bv[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) bv[k] = bnext[k];
-                if (kLBaseAhead > 1) {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) bnext[k] = bnext2[k];
-                    if (cs < 2) load_base(t, cs + 2, bnext2);
-                    else load_base(t + gridDim.x, cs - 2, bnext2);
-                } else {
-                    if (cs < 3) load_base(t, cs + 1, bnext);
-                    else load_base(t + gridDim.x, 0, bnext);
-                }
+                if (cs < kWSlices - 1) load_base(t, cs + 1, bnext);
+                else load_base(t + nunits, 0, bnext);
                 uint32_t acc[32];
                 tmem_ld_32x32b_x32(tmem_base + static_cast<uint32_t>(slot * kLN + cl) +
                                        (static_cast<uint32_t>(q * 32) << 16),
                                    acc);
                 tmem_ld_wait();
-                if (cs == 3) {                                   // accumulator slot consumed
+                if (cs == kWSlices - 1) {                        // accumulator slot consumed
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&tmem_empty[slot]);
+                    if (lane == 0) {
+                        if (kPair) mbar_arrive_remote(mapa_shared(smem_u32(&tmem_empty[slot]), 0), 1);
+                        else mbar_arrive(&tmem_empty[slot]);
+                    }
                 }
-                uint8_t* obuf = obase + (nslice & 1) * p.n_out * kSlice;
+                uint8_t* obuf = obase + (p.nbuf == 2 ? (nslice & 1) : 0) * p.n_out * kSlice;
                 const uint32_t orow = smem_u32(obuf) + static_cast<uint32_t>(row * (kLSlice * 2));
+                if (kGStore) {
+                    // the group's store thread has waited for the store that last read obuf
+                    named_bar_sync(1 + grp, 128);
+                } else {
+                    if (p.nbuf == 1 && lane == 0) bulk_wait_read0();   // single buffer: last store read it
+                    __syncwarp();
+                }
+#ifndef DFX_LC_KO_EPI   // knock-out: no epilogue arithmetic / staging stores
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {                 // 8 columns per 16-byte chunk
-                    const int c8 = kLSlice * cs + 8 * k;        // column within the warp's half
+                    const int c8 = kLSlice * cs + 8 * k;        // column within the warp's group
                     const float4 g0 = *reinterpret_cast<const float4*>(&gw[0][c8]);
                     const float4 g1 = *reinterpret_cast<const float4*>(&gw[0][c8 + 4]);
                     const float4 h0 = *reinterpret_cast<const float4*>(&gw[1][c8]);
                     const float4 h1 = *reinterpret_cast<const float4*>(&gw[1][c8 + 4]);
-                    const float4 b0 = *reinterpret_cast<const float4*>(&gw[2][c8]);
-                    const float4 b1 = *reinterpret_cast<const float4*>(&gw[2][c8 + 4]);
+                    float bb[8] = {};
+                    if (kBias) {
+                        const float4 b0 = *reinterpret_cast<const float4*>(&gw[2][c8]);
+                        const float4 b1 = *reinterpret_cast<const float4*>(&gw[2][c8 + 4]);
+                        bb[0] = b0.x; bb[1] = b0.y; bb[2] = b0.z; bb[3] = b0.w;
+                        bb[4] = b1.x; bb[5] = b1.y; bb[6] = b1.z; bb[7] = b1.w;
+                    }
                     const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
                     const float gm[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-                    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
                     const uint32_t bw[4] = {bv[k].x, bv[k].y, bv[k].z, bv[k].w};
                     // element pairs: every dtype rounding is one packed F2FP conversion of
                     // two values (RNE, identical to two scalar roundings), unpacked by shifts
@@ -314,7 +395,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
                         const uint32_t dw = LcT<T>::pack(__fadd_rn(v0, u0), __fadd_rn(v1, u1));
                         const uint32_t y0w = LcT<T>::pack(__fadd_rn(b0f, LcT<T>::lo(dw)),
                                                           __fadd_rn(b1f, LcT<T>::hi(dw)));
-                        o[0][e2] = p.bias ? LcT<T>::pack(__fadd_rn(LcT<T>::lo(y0w), bb[e]),
+                        o[0][e2] = kBias ? LcT<T>::pack(__fadd_rn(LcT<T>::lo(y0w), bb[e]),
                                                          __fadd_rn(LcT<T>::hi(y0w), bb[e + 1]))
                                           : y0w;
                         o[1][e2] = dw;
@@ -328,18 +409,33 @@ __global__ void __launch_bounds__(kLThreads, 1)
                                o[kind][0], o[kind][1], o[kind][2], o[kind][3]);
                     }
                 }
-                // the warp's 32 rows of the slice go out by its own TMA store; before the
-                // next slice reuses the other buffer, the store issued from it two slices
-                // ago must have read its smem
+#endif
+                // the warp's 32 rows of the slice go out by its own TMA store; with two
+                // buffers, before the next slice reuses the other buffer, the store issued
+                // from it two slices ago must have read its smem
                 fence_async_smem();
+#ifndef DFX_LC_KO_STORE
+                if (kGStore) {
+                    named_bar_sync(1 + grp, 128);                // the group's 128 rows staged
+                    if (q == 0 && lane == 0) {
+                        for (int oi = 0; oi < p.n_out; ++oi)
+                            tma_store_2d(&maps.out[oi], obuf + oi * kSlice, col0, m0);
+                        bulk_commit();
+                        if (p.nbuf == 2) bulk_wait_read1();
+                        else bulk_wait_read0();
+                    }
+                }
+#endif
                 __syncwarp();
-                if (lane == 0) {
+#ifndef DFX_LC_KO_STORE
+                if (!kGStore && lane == 0) {
                     for (int oi = 0; oi < p.n_out; ++oi)
                         tma_store_2d(&maps.out[oi], obuf + oi * kSlice + q * 32 * (kLSlice * 2),
                                      col0, m0 + 32 * q);
                     bulk_commit();
-                    bulk_wait_read1();
+                    if (p.nbuf == 2) bulk_wait_read1();
                 }
+#endif
                 __syncwarp();
             }
         }
@@ -347,14 +443,17 @@ __global__ void __launch_bounds__(kLThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (kPair) cluster_sync();      // the leader's MMAs wrote this CTA's TMEM
     if (warp == kWMma) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem_base);
+        if (kPair) tmem_dealloc_pair<512>(tmem_base);
+        else tmem_dealloc<512>(tmem_base);
     }
 }
 
-size_t lc_smem(int stages, int n_out) {
-    return size_t(stages) * (kAStage + kBStage) + size_t(4) * n_out * kSlice + 1024 + 256;
+size_t lc_smem(int stages, int n_out, int nbuf) {
+    return size_t(stages) * (kAStage + kBStage) + size_t(kGroups) * nbuf * n_out * kSlice + 1024 +
+           256;
 }
 
 }  // namespace
@@ -372,41 +471,74 @@ cudaError_t launch_lora_compose(int dt, const void* mid, const void* b, const vo
         p.slot[k] = -1;
         if (!outs[k]) continue;
         cudaError_t e = make_tmap_2d_sw(&maps.out[p.n_out], dt, outs[k], rows, d_out, d_out * 2,
-                                        kLSlice, 32, 64);      // one warp's 32 rows
+                                        kLSlice, kGStore ? kLM : 32, 64);   // a group's / warp's rows
         if (e != cudaSuccess) return e;
         p.slot[k] = p.n_out++;
     }
     if (p.n_out == 0) return cudaSuccess;
     cudaError_t e = make_tmap_2d(&maps.mid, dt, mid, rows, r, r * 2, kLK, kLM, true);
     if (e != cudaSuccess) return e;
-    e = make_tmap_2d(&maps.b, dt, b, d_out, r, r * 2, kLK, kLN, true);
+    e = make_tmap_2d(&maps.b, dt, b, d_out, r, r * 2, kLK, kBRows, true);
     if (e != cudaSuccess) return e;
     p.rows = rows;
     p.d_out = d_out;
     p.kb = static_cast<int>((r + kLK - 1) / kLK);
-    p.m_tiles = static_cast<int>((rows + kLM - 1) / kLM);
+    p.m_tiles = static_cast<int>((rows + kTileM - 1) / kTileM);
     p.tiles = static_cast<int>(p.m_tiles * ((d_out + kLN - 1) / kLN));
     const int sms = device_sm_count(), optin = device_smem_optin();
-    auto kern = dt == kBF16 ? lora_compose_kernel<__nv_bfloat16> : lora_compose_kernel<__half>;
+    // the bias add is a template switch: a per-element select would issue its FADD / F2FP /
+    // unpack whether or not a bias was passed
+    auto kern = dt == kBF16 ? (bias ? lora_compose_kernel<__nv_bfloat16, true>
+                                    : lora_compose_kernel<__nv_bfloat16, false>)
+                            : (bias ? lora_compose_kernel<__half, true> : lora_compose_kernel<__half, false>);
     cudaFuncAttributes fa{};
     e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return e;
     const size_t budget = size_t(optin) - fa.sharedSizeBytes;   // dynamic shared memory
-    p.stages = 4;
-    while (p.stages > 1 && lc_smem(p.stages, p.n_out) > budget) --p.stages;
-    if (p.stages < 2) return cudaErrorNotSupported;   // > 3 outputs at once
+    // double-buffered output staging while at least min_st operand stages fit beside it,
+    // else one staging buffer (each slice waits for its previous store to read it)
+    static const int min_st = [] {
+        const char* e = std::getenv("DFX_LC_MIN_STAGES");
+        return e ? std::atoi(e) : 3;
+    }();
+    p.nbuf = 2;
+    p.stages = kMaxStages;
+    while (p.stages > min_st && lc_smem(p.stages, p.n_out, 2) > budget) --p.stages;
+    if (lc_smem(p.stages, p.n_out, 2) > budget) {
+        p.nbuf = 1;
+        p.stages = kMaxStages;
+        while (p.stages > 2 && lc_smem(p.stages, p.n_out, 1) > budget) --p.stages;
+        if (lc_smem(p.stages, p.n_out, 1) > budget) return cudaErrorNotSupported;  // > 3 outputs
+    }
     p.s = s;
     p.g = g;
     p.bias = bias;
     p.base = base;
     p.fp16 = dt == kF16;
-    const size_t smem = lc_smem(p.stages, p.n_out);
+    const size_t smem = lc_smem(p.stages, p.n_out, p.nbuf);
     e = ensure_max_dyn_smem(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    const int grid = std::min(p.tiles, sms);
     prof_begin("lora_compose_tc", st);
-    kern<<<grid, kLThreads, smem, st>>>(maps, p);
+    if (kPair) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * std::min(p.tiles, sms / 2), 1, 1);
+        cfg.blockDim = dim3(kLThreads, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, maps, p);
+    } else {
+        kern<<<std::min(p.tiles, sms), kLThreads, smem, st>>>(maps, p);
+        e = cudaGetLastError();
+    }
     prof_end(st);
+    if (e != cudaSuccess) return e;
     if (launches) ++*launches;
     return cudaGetLastError();
 }

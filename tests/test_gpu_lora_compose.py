@@ -45,6 +45,8 @@ def _lora_bound(o, mid, B, want, dt):
 CASES = [  # rows, d_out, r, dt
     (1, 8, 8, 1), (37, 136, 16, 1), (128, 256, 64, 1), (200, 264, 72, 1), (129, 520, 384, 1),
     (64, 1024, 128, 2), (255, 392, 40, 2), (300, 776, 384, 1),
+    # several 256-row pair tiles, the last one's upper CTA entirely past the token tail
+    (520, 1032, 384, 1), (777, 264, 64, 2),
 ]
 
 

@@ -107,6 +107,7 @@ struct LcParams {
     const float* bias;      // nullable (values representable in the working dtype)
     const void* base;       // [rows, d_out], read by the epilogue through L1
     int fp16;
+    int v8;                 // base rows 32-byte aligned (d_out % 16 == 0): 256-bit loads
 };
 
 __device__ __forceinline__ void tma_store_2d(const void* desc, const void* smem_src, int32_t c0,
@@ -134,6 +135,14 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
     return r;
+}
+
+// 256-bit load (sm_100: LDG.256): two 16-byte pieces of one 32-byte sector pair per thread
+__device__ __forceinline__ void ldg_nc_v8(const void* p, uint4& a, uint4& b) {
+    asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z),
+                   "=r"(b.w)
+                 : "l"(p));
 }
 
 __device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
@@ -303,9 +312,15 @@ __global__ void __launch_bounds__(kLThreads, 1)
             v[0] = v[1] = v[2] = v[3] = make_uint4(0, 0, 0, 0);   // knock-out: no base stream
             (void)src; (void)c0;
 #else
+            if (p.v8) {      // rows 32-byte aligned: 32-byte pieces, whole or past d_out
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                v[k] = ldg_nc_v4(src + min(c0 + 8 * k, p.d_out - 8));
+                for (int k = 0; k < 4; k += 2)
+                    ldg_nc_v8(src + min(c0 + 8 * k, p.d_out - 16), v[k], v[k + 1]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    v[k] = ldg_nc_v4(src + min(c0 + 8 * k, p.d_out - 8));
+            }
 #endif
         };
         uint4 bnext[4];
@@ -515,6 +530,9 @@ cudaError_t launch_lora_compose(int dt, const void* mid, const void* b, const vo
     p.bias = bias;
     p.base = base;
     p.fp16 = dt == kF16;
+#ifndef DFX_LC_NO_V8
+    p.v8 = d_out % 16 == 0 && reinterpret_cast<uintptr_t>(base) % 32 == 0;
+#endif
     const size_t smem = lc_smem(p.stages, p.n_out, p.nbuf);
     e = ensure_max_dyn_smem(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
     if (e != cudaSuccess) return e;

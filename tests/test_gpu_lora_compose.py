@@ -47,6 +47,8 @@ CASES = [  # rows, d_out, r, dt
     (64, 1024, 128, 2), (255, 392, 40, 2), (300, 776, 384, 1),
     # several 256-row pair tiles, the last one's upper CTA entirely past the token tail
     (520, 1032, 384, 1), (777, 264, 64, 2),
+    # d_out % 16 == 0 with a 16-column last tile (the 256-bit base loads' tail)
+    (200, 272, 72, 1), (333, 1040, 384, 2),
 ]
 
 

@@ -139,7 +139,11 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
 
 // 256-bit load (sm_100: LDG.256): two 16-byte pieces of one 32-byte sector pair per thread
 __device__ __forceinline__ void ldg_nc_v8(const void* p, uint4& a, uint4& b) {
+#ifndef DFX_LC_V8_ALLOC   // no L1 allocation: the pieces use whole sectors, never re-read
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+#else
     asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+#endif
                  : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z),
                    "=r"(b.w)
                  : "l"(p));

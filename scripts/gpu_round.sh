@@ -15,4 +15,14 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:"tc_
     -o gpurun_out/${R}_ncu_norm python scripts/profile_module.py --steps 2 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:tc_pair_rowdot -s 1 -c 1 \
     -o gpurun_out/${R}_ncu_tc_pair_rowdot_budget104 python scripts/profile_module.py --steps 3 --budget 104 > /dev/null 2>&1
+# the composes and the fused LoRA-up + compose kernel, and the bench's own launch list
+for k in compose_fwd_vec compose_bwd_serial; do
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
+      -o gpurun_out/${R}_ncu_$k python scripts/profile_module.py --steps 3 --bwd > /dev/null 2>&1
+done
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:lora_compose -s 2 -c 1 \
+    -o gpurun_out/${R}_ncu_lora_compose python scripts/exp_kernels.py --what lora_fused --iters 1 > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file gpurun_out/${R}_bench_launches.csv python bench.py --steps 40 --warmup 3 --no-cpu-baseline \
+    --e2e-steps 1 --lora-steps 2 --variant-steps 40 > /dev/null 2>&1
 ls gpurun_out | grep $R

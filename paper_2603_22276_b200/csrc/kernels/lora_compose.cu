@@ -149,6 +149,18 @@ __device__ __forceinline__ void ldg_nc_v8(const void* p, uint4& a, uint4& b) {
                  : "l"(p));
 }
 
+// Two RN fp32 products in one packed FMUL2 (mul.rn.f32x2): bitwise two __fmul_rn.  Only the
+// products use it; every add stays a scalar add.rn (a packed add after a packed mul is
+// contracted into FFMA2 by ptxas, see compose.cu).
+__device__ __forceinline__ void lc_fmul2(float a0, float a1, float b0, float b1, float& d0, float& d1) {
+    const uint64_t a = (uint64_t(__float_as_uint(a1)) << 32) | __float_as_uint(a0);
+    const uint64_t b = (uint64_t(__float_as_uint(b1)) << 32) | __float_as_uint(b0);
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    d0 = __uint_as_float(static_cast<uint32_t>(d));
+    d1 = __uint_as_float(static_cast<uint32_t>(d >> 32));
+}
+
 __device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                        uint32_t d) {
     asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
@@ -408,9 +420,16 @@ __global__ void __launch_bounds__(kLThreads, 1)
                         const uint32_t lw = LcT<T>::pack(__uint_as_float(acc[8 * k + e]),
                                                          __uint_as_float(acc[8 * k + e + 1]));
                         const float l0 = LcT<T>::lo(lw), l1 = LcT<T>::hi(lw);
+#ifdef DFX_LC_FMUL2
+                        float t0, t1, u0, u1, v0, v1;
+                        lc_fmul2(sf, sf, l0, l1, t0, t1);
+                        lc_fmul2(gv[e], gv[e + 1], t0, t1, u0, u1);
+                        lc_fmul2(gm[e], gm[e + 1], b0f, b1f, v0, v1);
+#else
                         const float t0 = __fmul_rn(sf, l0), t1 = __fmul_rn(sf, l1);
                         const float u0 = __fmul_rn(gv[e], t0), u1 = __fmul_rn(gv[e + 1], t1);
                         const float v0 = __fmul_rn(gm[e], b0f), v1 = __fmul_rn(gm[e + 1], b1f);
+#endif
                         const uint32_t dw = LcT<T>::pack(__fadd_rn(v0, u0), __fadd_rn(v1, u1));
                         const uint32_t y0w = LcT<T>::pack(__fadd_rn(b0f, LcT<T>::lo(dw)),
                                                           __fadd_rn(b1f, LcT<T>::hi(dw)));

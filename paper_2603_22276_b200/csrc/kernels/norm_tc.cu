@@ -1851,7 +1851,18 @@ cudaError_t launch_norm_tc(const NormArgs& a, Workspace* ws, cudaStream_t st, in
             p.Z = a.b; p.ldz = r; p.out = ba; p.out_scale = inv_scale;
             p.tiles = static_cast<int>(pm_tiles);
             set_fin(p);
-            e = launch_gstat(tb, tg, p, plan.b_ctas / 2, vs, el);
+            // Measurement switches: DFX_V_HALF=1 runs V on half the planned pairs under an SM
+            // budget (two tiles each, G slice resident, the other SMs left to the compose
+            // stream), DFX_V_PAIRS=n caps the pairs.  C2 training +0.3-1 %, but C3 -2.5 / -8 %
+            // and the C5 stack -18 % (profiles/r02_v_pairs_sweep.txt): off.
+            static const int v_cap = env_int("DFX_V_PAIRS", 0);
+            static const int v_half = env_int("DFX_V_HALF", 0);
+            const int nsl = std::max(1, gstat_shape(r).nsl);
+            int v_pairs = plan.b_ctas / 2;
+            if (v_cap > 0) v_pairs = std::min(v_cap, v_pairs);
+            else if (v_half && sms < device_sm_count())
+                v_pairs = std::max(nsl, v_pairs / 2 / nsl * nsl);
+            e = launch_gstat(tb, tg, p, v_pairs, vs, el);
             if (e == cudaSuccess && launches) ++*launches;
             return e;
         }

@@ -87,6 +87,11 @@ constexpr int kMaxStages = kPair ? 6 : 4;
 constexpr int kSlice = kLM * kLSlice * 2;     // 8 KiB
 constexpr int kWCols = kLN / kGroups;         // columns of a tile per epilogue warp
 constexpr int kWSlices = kWCols / kLSlice;    // 32-column slices per warp and tile
+#ifdef DFX_LC_TMEM_X16
+constexpr int kAccCols = 16;                   // accumulator columns per tcgen05.ld
+#else
+constexpr int kAccCols = 32;
+#endif
 constexpr int kMaxOut = 4;                    // y, delta, inner, lora
 
 struct LcMaps {
@@ -370,19 +375,26 @@ __global__ void __launch_bounds__(kLThreads, 1)
                 for (int k = 0; k < 4; ++k) bv[k] = bnext[k];
                 if (cs < kWSlices - 1) load_base(t, cs + 1, bnext);
                 else load_base(t + nunits, 0, bnext);
-                uint32_t acc[32];
-                tmem_ld_32x32b_x32(tmem_base + static_cast<uint32_t>(slot * kLN + cl) +
-                                       (static_cast<uint32_t>(q * 32) << 16),
-                                   acc);
-                tmem_ld_wait();
-                if (cs == kWSlices - 1) {                        // accumulator slot consumed
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (kPair) mbar_arrive_remote(mapa_shared(smem_u32(&tmem_empty[slot]), 0), 1);
-                        else mbar_arrive(&tmem_empty[slot]);
+                // the slice's accumulator columns, all 32 at once or in two 16-column halves
+                // (DFX_LC_TMEM_X16: 16 fewer registers per thread)
+                uint32_t acc[kAccCols];
+                auto load_acc = [&](int c) {
+                    const uint32_t ta = tmem_base + static_cast<uint32_t>(slot * kLN + cl + c) +
+                                        (static_cast<uint32_t>(q * 32) << 16);
+                    if constexpr (kAccCols == 32)
+                        tmem_ld_32x32b_x32(ta, *reinterpret_cast<uint32_t(*)[32]>(acc));
+                    else
+                        tmem_ld_32x32b_x16(ta, *reinterpret_cast<uint32_t(*)[16]>(acc));
+                    tmem_ld_wait();
+                    if (cs == kWSlices - 1 && c + kAccCols == kLSlice) {   // slot consumed
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (kPair) mbar_arrive_remote(mapa_shared(smem_u32(&tmem_empty[slot]), 0), 1);
+                            else mbar_arrive(&tmem_empty[slot]);
+                        }
                     }
-                }
+                };
                 uint8_t* obuf = obase + (p.nbuf == 2 ? (nslice & 1) : 0) * p.n_out * kSlice;
                 const uint32_t orow = smem_u32(obuf) + static_cast<uint32_t>(row * (kLSlice * 2));
                 if (kGStore) {
@@ -392,9 +404,10 @@ __global__ void __launch_bounds__(kLThreads, 1)
                     if (p.nbuf == 1 && lane == 0) bulk_wait_read0();   // single buffer: last store read it
                     __syncwarp();
                 }
-#ifndef DFX_LC_KO_EPI   // knock-out: no epilogue arithmetic / staging stores
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {                 // 8 columns per 16-byte chunk
+                    if ((8 * k) % kAccCols == 0) load_acc(8 * k);
+#ifndef DFX_LC_KO_EPI   // knock-out: no epilogue arithmetic / staging stores
                     const int c8 = kLSlice * cs + 8 * k;        // column within the warp's group
                     const float4 g0 = *reinterpret_cast<const float4*>(&gw[0][c8]);
                     const float4 g1 = *reinterpret_cast<const float4*>(&gw[0][c8 + 4]);
@@ -417,8 +430,9 @@ __global__ void __launch_bounds__(kLThreads, 1)
                     for (int e2 = 0; e2 < 4; ++e2) {
                         const int e = 2 * e2;
                         const float b0f = LcT<T>::lo(bw[e2]), b1f = LcT<T>::hi(bw[e2]);
-                        const uint32_t lw = LcT<T>::pack(__uint_as_float(acc[8 * k + e]),
-                                                         __uint_as_float(acc[8 * k + e + 1]));
+                        const int ai = (8 * k) % kAccCols + e;
+                        const uint32_t lw = LcT<T>::pack(__uint_as_float(acc[ai]),
+                                                         __uint_as_float(acc[ai + 1]));
                         const float l0 = LcT<T>::lo(lw), l1 = LcT<T>::hi(lw);
 #ifdef DFX_LC_FMUL2
                         float t0, t1, u0, u1, v0, v1;
@@ -446,8 +460,8 @@ __global__ void __launch_bounds__(kLThreads, 1)
                         sts_v4(orow + static_cast<uint32_t>(p.slot[kind] * kSlice + ((k ^ sw) << 4)),
                                o[kind][0], o[kind][1], o[kind][2], o[kind][3]);
                     }
-                }
 #endif
+                }
                 // the warp's 32 rows of the slice go out by its own TMA store; with two
                 // buffers, before the next slice reuses the other buffer, the store issued
                 // from it two slices ago must have read its smem

@@ -25,10 +25,12 @@
 // 0-3 take column slices 0-1 of a tile, warps 4-7 slices 2-3), 8 operand producer,
 // 9 MMA issuer.
 //
-// Measured alternatives kept as compile-time switches, all parity-green and all slower at C2
-// (profiles/r02_lora_epilogue_sweep.txt): DFX_LC_EPI_WARPS=16, DFX_LC_PAIR=1 (CTA pairs, half
-// of B per CTA), DFX_LC_GSTORE=1 (one 128-row TMA store per column group).  Knock-out
-// switches DFX_LC_KO_{BASE,STORE,MMA,EPI} split the kernel's time.
+// Default build (profiles/r02_lora_epilogue_sweep.txt): CTA pairs (DFX_LC_PAIR: M = 256, each
+// CTA stages half of B) and, when d_out % 16 == 0 and the outputs are 32-byte aligned, outputs
+// stored straight from registers as 256-bit no-allocate stores (DFX_LC_DIRECT); otherwise the
+// smem-staged TMA stores below.  Measured slower and kept as switches, all parity-green:
+// DFX_LC_EPI_WARPS=16 (+ DFX_LC_TMEM_X16), DFX_LC_GSTORE=1, DFX_LC_FMUL2.  Knock-out switches
+// DFX_LC_KO_{BASE,STORE,MMA,EPI} split the kernel's time.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -65,7 +67,7 @@ __device__ __forceinline__ void lc_wait(uint64_t* bar, uint32_t phase) {
 constexpr int kWProd = kEpiWarps, kWMma = kEpiWarps + 1;
 constexpr int kAStage = kLM * kLK * 2;        // 16 KiB of mid
 #ifndef DFX_LC_PAIR
-#define DFX_LC_PAIR 0
+#define DFX_LC_PAIR 1
 #endif
 #ifndef DFX_LC_GSTORE
 #define DFX_LC_GSTORE 0
@@ -113,6 +115,8 @@ struct LcParams {
     const void* base;       // [rows, d_out], read by the epilogue through L1
     int fp16;
     int v8;                 // base rows 32-byte aligned (d_out % 16 == 0): 256-bit loads
+    int direct;             // outputs stored from registers (256-bit, no smem staging)
+    void* outp[kMaxOut];    // enabled outputs' base pointers, compacted like the maps
 };
 
 __device__ __forceinline__ void tma_store_2d(const void* desc, const void* smem_src, int32_t c0,
@@ -164,6 +168,13 @@ __device__ __forceinline__ void lc_fmul2(float a0, float a1, float b0, float b1,
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
     d0 = __uint_as_float(static_cast<uint32_t>(d));
     d1 = __uint_as_float(static_cast<uint32_t>(d >> 32));
+}
+
+// 256-bit store without L1 allocation: 32 bytes of one row per thread
+__device__ __forceinline__ void stg_na_v8(void* p, const uint32_t (&a)[4], const uint32_t (&b)[4]) {
+    asm volatile("st.global.L1::no_allocate.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p),
+                 "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3])
+                 : "memory");
 }
 
 __device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
@@ -378,6 +389,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
                 // the slice's accumulator columns, all 32 at once or in two 16-column halves
                 // (DFX_LC_TMEM_X16: 16 fewer registers per thread)
                 uint32_t acc[kAccCols];
+                uint32_t oprev[kMaxOut][4];                 // direct stores: the even chunk
                 auto load_acc = [&](int c) {
                     const uint32_t ta = tmem_base + static_cast<uint32_t>(slot * kLN + cl + c) +
                                         (static_cast<uint32_t>(q * 32) << 16);
@@ -401,7 +413,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
                     // the group's store thread has waited for the store that last read obuf
                     named_bar_sync(1 + grp, 128);
                 } else {
-                    if (p.nbuf == 1 && lane == 0) bulk_wait_read0();   // single buffer: last store read it
+                    if (p.nbuf == 1 && !p.direct && lane == 0) bulk_wait_read0();   // single buffer: last store read it
                     __syncwarp();
                 }
 #pragma unroll
@@ -454,20 +466,42 @@ __global__ void __launch_bounds__(kLThreads, 1)
                         o[2][e2] = LcT<T>::pack(__fadd_rn(t0, b0f), __fadd_rn(t1, b1f));
                         o[3][e2] = lw;
                     }
+                    if (p.direct) {
+                        // two chunks (16 columns, 32 bytes) per 256-bit store of this row; rows
+                        // past the token tail and 16-column pieces past d_out are not written
+                        if (k & 1) {
+                            const int64_t gr = int64_t(m0) + row;
+                            const int64_t gc = int64_t(col0) + 8 * (k - 1);
+                            if (gr < p.rows && gc < p.d_out) {
+#pragma unroll
+                                for (int kind = 0; kind < kMaxOut; ++kind) {
+                                    if (p.slot[kind] < 0) continue;
+                                    T* dst = static_cast<T*>(p.outp[p.slot[kind]]) + gr * p.d_out + gc;
+                                    stg_na_v8(dst, oprev[kind], o[kind]);
+                                }
+                            }
+                        } else {
+#pragma unroll
+                            for (int kind = 0; kind < kMaxOut; ++kind)
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) oprev[kind][i] = o[kind][i];
+                        }
+                    } else {
 #pragma unroll
                     for (int kind = 0; kind < kMaxOut; ++kind) {
                         if (p.slot[kind] < 0) continue;      // output not requested (uniform)
                         sts_v4(orow + static_cast<uint32_t>(p.slot[kind] * kSlice + ((k ^ sw) << 4)),
                                o[kind][0], o[kind][1], o[kind][2], o[kind][3]);
                     }
+                    }
 #endif
                 }
                 // the warp's 32 rows of the slice go out by its own TMA store; with two
                 // buffers, before the next slice reuses the other buffer, the store issued
                 // from it two slices ago must have read its smem
-                fence_async_smem();
+                if (!p.direct) fence_async_smem();
 #ifndef DFX_LC_KO_STORE
-                if (kGStore) {
+                if (kGStore && !p.direct) {
                     named_bar_sync(1 + grp, 128);                // the group's 128 rows staged
                     if (q == 0 && lane == 0) {
                         for (int oi = 0; oi < p.n_out; ++oi)
@@ -480,7 +514,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
 #endif
                 __syncwarp();
 #ifndef DFX_LC_KO_STORE
-                if (!kGStore && lane == 0) {
+                if (!kGStore && !p.direct && lane == 0) {
                     for (int oi = 0; oi < p.n_out; ++oi)
                         tma_store_2d(&maps.out[oi], obuf + oi * kSlice + q * 32 * (kLSlice * 2),
                                      col0, m0 + 32 * q);
@@ -525,6 +559,7 @@ cudaError_t launch_lora_compose(int dt, const void* mid, const void* b, const vo
         cudaError_t e = make_tmap_2d_sw(&maps.out[p.n_out], dt, outs[k], rows, d_out, d_out * 2,
                                         kLSlice, kGStore ? kLM : 32, 64);   // a group's / warp's rows
         if (e != cudaSuccess) return e;
+        p.outp[p.n_out] = outs[k];
         p.slot[k] = p.n_out++;
     }
     if (p.n_out == 0) return cudaSuccess;
@@ -553,10 +588,21 @@ cudaError_t launch_lora_compose(int dt, const void* mid, const void* b, const vo
         const char* e = std::getenv("DFX_LC_MIN_STAGES");
         return e ? std::atoi(e) : 3;
     }();
-    p.nbuf = 2;
+#ifndef DFX_LC_DIRECT
+#define DFX_LC_DIRECT 1
+#endif
+    // outputs straight from registers (256-bit stores, no staging) when every output row is
+    // 32-byte aligned
+    p.direct = 0;
+    if (DFX_LC_DIRECT && d_out % 16 == 0) {
+        p.direct = 1;
+        for (int k = 0; k < p.n_out; ++k)
+            if (reinterpret_cast<uintptr_t>(p.outp[k]) % 32 != 0) p.direct = 0;
+    }
+    p.nbuf = p.direct ? 0 : 2;
     p.stages = kMaxStages;
-    while (p.stages > min_st && lc_smem(p.stages, p.n_out, 2) > budget) --p.stages;
-    if (lc_smem(p.stages, p.n_out, 2) > budget) {
+    while (p.stages > min_st && lc_smem(p.stages, p.n_out, p.nbuf) > budget) --p.stages;
+    if (!p.direct && lc_smem(p.stages, p.n_out, 2) > budget) {
         p.nbuf = 1;
         p.stages = kMaxStages;
         while (p.stages > 2 && lc_smem(p.stages, p.n_out, 1) > budget) --p.stages;

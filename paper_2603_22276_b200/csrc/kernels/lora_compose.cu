@@ -161,6 +161,7 @@ __device__ __forceinline__ void ldg_nc_v8(const void* p, uint4& a, uint4& b) {
 // Two RN fp32 products in one packed FMUL2 (mul.rn.f32x2): bitwise two __fmul_rn.  Only the
 // products use it; every add stays a scalar add.rn (a packed add after a packed mul is
 // contracted into FFMA2 by ptxas, see compose.cu).
+#ifdef DFX_LC_FMUL2
 __device__ __forceinline__ void lc_fmul2(float a0, float a1, float b0, float b1, float& d0, float& d1) {
     const uint64_t a = (uint64_t(__float_as_uint(a1)) << 32) | __float_as_uint(a0);
     const uint64_t b = (uint64_t(__float_as_uint(b1)) << 32) | __float_as_uint(b0);
@@ -169,6 +170,7 @@ __device__ __forceinline__ void lc_fmul2(float a0, float a1, float b0, float b1,
     d0 = __uint_as_float(static_cast<uint32_t>(d));
     d1 = __uint_as_float(static_cast<uint32_t>(d >> 32));
 }
+#endif
 
 // 256-bit store without L1 allocation: 32 bytes of one row per thread
 __device__ __forceinline__ void stg_na_v8(void* p, const uint32_t (&a)[4], const uint32_t (&b)[4]) {

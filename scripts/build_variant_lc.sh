@@ -4,7 +4,7 @@ set -e
 cd "$(dirname "$0")/.."
 NAME=$1; FLAGS=$2
 C=paper_2603_22276_b200/csrc
-make -s -C $C ../libdfx.so
+make -s -C $C
 mkdir -p variants/obj_$NAME
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
      -Iinclude -I$C/kernels $FLAGS -c $C/kernels/lora_compose.cu -o variants/obj_$NAME/lora_compose.o

@@ -655,12 +655,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int64_t m0 = int64_t(t / p.n_split) * (2 * kBM) + int64_t(rank) * kBM;
                 const int64_t n0 = int64_t(t % p.n_split) * bn_pair + int64_t(rank) * half_n;
                 // W streams from HBM in 128-byte row pieces: warm L2 `pf` K blocks ahead
-                for (int it = 0; it < pf && it < nkb_blocks; ++it)
-                    tma_prefetch_2d(&tmx, (kb0 + it) * kBK, static_cast<int32_t>(m0));
+                // (W's map is the 3-D K-atom view when p.tma3d: prefetch with its coordinates;
+                // a 2-D prefetch on a 3-D map is an illegal instruction)
+                auto prefetch_w = [&](int64_t kb) {
+                    if (p.tma3d) tma_prefetch_3d(&tmx, 0, static_cast<int32_t>(m0), static_cast<int32_t>(kb));
+                    else tma_prefetch_2d(&tmx, static_cast<int32_t>(kb * kBK), static_cast<int32_t>(m0));
+                };
+                for (int it = 0; it < pf && it < nkb_blocks; ++it) prefetch_w(kb0 + it);
                 for (int it = 0; it < nkb; ++it) {
                     for (int a = 0; a < ka; ++a)
-                        if (pf > 0 && it * ka + a + pf < nkb_blocks)
-                            tma_prefetch_2d(&tmx, (kb0 + it * ka + a + pf) * kBK, static_cast<int32_t>(m0));
+                        if (pf > 0 && it * ka + a + pf < nkb_blocks) prefetch_w(kb0 + it * ka + a + pf);
                     mbar_wait(&empty[s], ph ^ 1);
                     DFX_TR(3, it);
                     if (leader) mbar_arrive_expect_tx(&full[s], 2 * stage_bytes);

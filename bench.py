@@ -347,8 +347,12 @@ def run_gpu(args, rank, world, local_rank, dist):
         if args.only != "norm":
             compose(b, mode)
 
-    stream = torch.cuda.Stream(device=dev)
-    side = torch.cuda.Stream(device=dev)
+    # --stream-priority (measurement): a higher CUDA stream priority (-1) for the compose
+    # stream or the norm stream of the pipelined graphs
+    prio_c = -1 if args.stream_priority == "compose" else 0
+    prio_n = -1 if args.stream_priority == "norm" else 0
+    stream = torch.cuda.Stream(device=dev, priority=prio_n)
+    side = torch.cuda.Stream(device=dev, priority=prio_c)
     third = torch.cuda.Stream(device=dev)
     # Every dfx call below issues on torch's current stream: make that `stream` for the whole
     # run.  Calls on one context must not overlap (dfx.h: the workspace is shared), and torch's
@@ -1222,6 +1226,8 @@ def main():
     ap.add_argument("--prof-steps", type=int, default=40)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stream-priority", default="none", choices=["none", "compose", "norm"],
+                    help="measurement: raise the compose or the norm stream's CUDA priority")
     ap.add_argument("--no-cpu-full-module", action="store_true",
                     help="skip the one whole module on one core that validates the CPU model")
     ap.add_argument("--pipeline", type=int, default=40,
